@@ -1,0 +1,123 @@
+/*
+ * isrs_egn.h — C ABI of the B200-native ISRS EGN hot path (paper arXiv 2412.11614).
+ *
+ * What it computes (PAPER.md = /root/reference/PAPER.md, P:n = line n):
+ *   eta_kappa = sigma^2_NLI,kappa / P_kappa^3                     Eq. 11
+ * for every requested channel of interest (COI) kappa, with sigma^2 assembled from the
+ * ISRS EGN island integrals D, E, F, G, H (Eqs. 15-21) over the 2-D (f1, f2)
+ * domain at f = f_kappa (reading C1 of DESIGN.md), the link function Y (Eq. 22, P:267,
+ * reading C3: phase of the preceding spans, gain products = 1), and the FWM efficiency
+ * factor mu_s in the paper's segment closed form (Eqs. 7-10).
+ * Readings C1-C17 fix everything the paper leaves open; the oracle in
+ * oracle/ implements the same definition independently.
+ *
+ * Units: SI throughout (Hz, W, m, s^2/m, s^3/m, 1/(W m), 1/(W m Hz)); frequencies absolute.
+ * Exactness requirement (reading C10): every f_center_hz and symbol_rate_hz is an integer
+ * number of Hz, and symbol_rate_hz / (2 * grid_n) is an integer, so that every grid frequency
+ * and every f1 + f2 - f is exact in fp64 and band-edge ties are decided exactly.
+ *
+ * Threading: a handle is not thread-safe; distinct handles are independent.
+ * Errors: every call returns a status; on error nothing is enqueued and outputs are untouched;
+ * isrs_egn_last_error() (thread-local) names the offending field / index.
+ */
+#ifndef ISRS_EGN_H
+#define ISRS_EGN_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define ISRS_EGN_API __attribute__((visibility("default")))
+#else
+#define ISRS_EGN_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct isrs_egn isrs_egn_t; /* opaque handle; owns all device memory */
+
+enum {
+  ISRS_EGN_OK = 0,
+  ISRS_EGN_EINVAL = -1,      /* bad argument: non-finite, out of range, not on the Hz lattice */
+  ISRS_EGN_EOVERLAP = -2,    /* channel bands [f - R/2, f + R/2] overlap (touching is allowed) */
+  ISRS_EGN_ERANGE = -3,      /* B_tot * zeta overflows sinh, or K_s / table too large           */
+  ISRS_EGN_ENOMEM = -4,      /* device or host allocation failed                                */
+  ISRS_EGN_ECUDA = -5,       /* any CUDA error (asynchronous ones surface at the next call)     */
+  ISRS_EGN_EUNSUPPORTED = -6 /* precision / mu_mode not available                               */
+};
+
+/* Link description.  create() deep-copies every array; the caller may free them on return. */
+typedef struct {
+  int32_t n_ch;                    /* >= 1                                                    */
+  const double *f_center_hz;       /* [n_ch] strictly increasing, integer Hz                  */
+  const double *symbol_rate_hz;    /* [n_ch] R_i > 0, integer Hz; band = [f - R/2, f + R/2]   */
+  const double *launch_power_w;    /* [n_ch] P_i > 0                                          */
+  const double *excess_kurtosis;   /* [n_ch] Phi_i (Gaussian 0, QPSK -1), Eq. 15 (reading C9) */
+  const double *psi;               /* [n_ch] Psi_i sixth-order factor, or NULL (=> 0)         */
+  int32_t n_span;                  /* >= 1                                                    */
+  const double *length_m;          /* [n_span] L_s > 0                                        */
+  const double *alpha_per_m;       /* [n_span] power attenuation alpha_s > 0 (Eq. 9 divides by i chi - alpha) */
+  const double *beta2_s2_per_m;    /* [n_span] at the band centre f_c (readings C5, C15)      */
+  const double *beta3_s3_per_m;    /* [n_span]                                                */
+  const double *gamma_per_w_m;     /* [n_span] >= 0                                           */
+  const double *cr_per_w_m_hz;     /* [n_span] Raman gain slope C_r >= 0 (0.028/W/km/THz = 2.8e-17) */
+} isrs_egn_problem;
+
+enum { ISRS_EGN_MU_SEGMENT = 0,    /* Eqs. 8-10 (default, the hot path)                       */
+       ISRS_EGN_MU_MACLAURIN = 1   /* Eq. 4 (NEXT-1)                                          */ };
+
+enum { ISRS_EGN_FLAG_UNIT_LINK = 1u /* test hook: Y := 1 (oracle pin P6)                     */ };
+
+typedef struct {
+  int32_t grid_n;      /* N: N x N bin-centre grid per (kappa1, kappa2) region; even, >= 2 (C6) */
+  double delta_z_m;    /* segment step; K_s = ceil(L_s / delta_z_m); paper default 1000 */
+  int32_t precision;   /* 64 (fp64, default) | 32 (mixed fp32 variant, row a8)                  */
+  int32_t mu_mode;     /* ISRS_EGN_MU_*                                                          */
+  uint32_t flags;      /* ISRS_EGN_FLAG_*                                                        */
+} isrs_egn_numerics;
+
+/* Validate, canonicalise (f_c, B_tot, P_tot, K_s; reading C5), enumerate the regions of every
+ * channel and run the per-span ISRS profile precompute on `device` (synchronous). */
+ISRS_EGN_API int isrs_egn_create(const isrs_egn_problem *p, const isrs_egn_numerics *n, int device,
+                    isrs_egn_t **out);
+
+/* eta for n_coi COIs (coi: HOST array of channel indices, NULL = all channels 0..n_ch-1 with
+ * n_coi = n_ch).  eta_dev: DEVICE [n_coi] (1/W^2).  terms_dev: DEVICE [n_coi * 5] contributions
+ * of D, E, F, G, H to eta (row-major) or NULL.  Enqueued on cuda_stream (cudaStream_t; NULL =
+ * legacy default stream); results are valid after the stream synchronises.  Deterministic:
+ * bitwise-identical results across calls. */
+ISRS_EGN_API int isrs_egn_nli(isrs_egn_t *h, int32_t n_coi, const int32_t *coi, double *eta_dev,
+                 double *terms_dev, void *cuda_stream);
+
+/* Per-region partial integrals written by the most recent isrs_egn_nli() call (synchronises
+ * the handle's last stream).  For each query q: region (kappa[q], k1[q], k2[q]) ->
+ * out_host[6q .. 6q+5] = { D_w, E_w, F_w, G_w, H_w, n_points } with
+ *   D_w = sum_islands G_k3 D,  E_w = E[k3 == k1],  F_w = F[k3 == k2],
+ *   G_w = sum_islands G_k3 G [k1 == k2],  H_w = H[k1 == k2 == k3]
+ * (raw integrals of Eqs. 17-21 in the PSD normalisation of reading C2; a term whose gate or
+ * Phi/Psi weight is zero is not evaluated and reads 0).  A region outside the last call's
+ * work list reads as all zeros with n_points = -1. */
+ISRS_EGN_API int isrs_egn_region_partials(isrs_egn_t *h, int32_t n, const int32_t *kappa, const int32_t *k1,
+                             const int32_t *k2, double *out_host);
+
+/* Work of the most recent isrs_egn_nli() call (synchronises): in-support grid points summed
+ * over COIs and regions, point-spans = points * n_span, and the number of regions launched. */
+ISRS_EGN_API int isrs_egn_work(isrs_egn_t *h, int64_t *points, int64_t *point_spans, int64_t *regions);
+
+/* One-shot end-to-end call with HOST buffers: create + nli (all given COIs) + copy back +
+ * destroy.  eta_host [n_coi], terms_host [n_coi * 5] or NULL. */
+ISRS_EGN_API int isrs_egn_eta_host(const isrs_egn_problem *p, const isrs_egn_numerics *n, int device,
+                      int32_t n_coi, const int32_t *coi, double *eta_host, double *terms_host);
+
+/* Number of kernel launches the most recent isrs_egn_nli() enqueued (for bench accounting). */
+ISRS_EGN_API int isrs_egn_last_launch_count(const isrs_egn_t *h);
+
+ISRS_EGN_API void isrs_egn_destroy(isrs_egn_t *h); /* NULL-safe; synchronises the device */
+ISRS_EGN_API const char *isrs_egn_strerror(int code);
+ISRS_EGN_API const char *isrs_egn_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ISRS_EGN_H */

@@ -1,0 +1,121 @@
+"""B200-native ISRS EGN hot path (arXiv 2412.11614): eta(f_COI) per channel with the segment
+closed-form FWM efficiency factor, span phased-array sum and EGN corrections, in sm_100a
+kernels behind the C ABI of include/isrs_egn.h.
+
+Python here only marshals arguments; PyTorch is used only for device memory and streams.
+
+    h = Engine(link)                 # isrs_egn_create
+    eta = h.nli()                    # isrs_egn_nli -> torch.float64 CUDA tensor [n_coi] (1/W^2)
+    h.close()                        # isrs_egn_destroy
+"""
+import ctypes
+
+import numpy as np
+
+from . import _abi
+from ._abi import (FLAG_UNIT_LINK, MU_MACLAURIN, MU_SEGMENT, IsrsEgnError, ProblemArrays,  # noqa: F401
+                   numerics)
+
+__all__ = ["Engine", "eta_host", "IsrsEgnError", "MU_SEGMENT", "MU_MACLAURIN", "FLAG_UNIT_LINK",
+           "library_path"]
+
+
+def library_path():
+    return _abi.LIB_PATH
+
+
+class Engine:
+    """Handle over one link (isrs_egn_create / isrs_egn_nli / isrs_egn_destroy)."""
+
+    def __init__(self, link, grid_n=None, delta_z_m=None, device=0, precision=64,
+                 mu_mode=MU_SEGMENT, flags=0):
+        self._pa = ProblemArrays(link)
+        n = numerics(grid_n if grid_n is not None else link.grid_n,
+                     delta_z_m if delta_z_m is not None else getattr(link, "delta_z_m", 1000.0),
+                     precision, mu_mode, flags)
+        self.n_ch = self._pa.struct.n_ch
+        self.n_span = self._pa.struct.n_span
+        self.device = device
+        h = ctypes.c_void_p()
+        _abi.check(_abi.lib.isrs_egn_create(ctypes.byref(self._pa.struct), ctypes.byref(n), device,
+                                            ctypes.byref(h)))
+        self._h = h
+
+    def nli_into(self, eta_ptr, terms_ptr=0, coi=None, stream=0):
+        """Raw call: device pointers (ints) and a cudaStream_t handle (int)."""
+        if coi is None:
+            n, cp = self.n_ch, None
+        else:
+            c = np.ascontiguousarray(np.asarray(coi, dtype=np.int32))
+            n, cp = len(c), c.ctypes.data_as(_abi._ip)
+            self._coi_keep = c
+        _abi.check(_abi.lib.isrs_egn_nli(self._h, n, cp, ctypes.c_void_p(eta_ptr),
+                                         ctypes.c_void_p(terms_ptr or None),
+                                         ctypes.c_void_p(stream or None)))
+
+    def nli(self, coi=None, terms=False, stream=None):
+        """eta [n_coi] (and the D, E, F, G, H breakdown [n_coi, 5]) as float64 CUDA tensors."""
+        import torch
+        n = self.n_ch if coi is None else len(coi)
+        dev = torch.device("cuda", self.device)
+        eta = torch.empty(n, dtype=torch.float64, device=dev)
+        tt = torch.empty((n, 5), dtype=torch.float64, device=dev) if terms else None
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        self.nli_into(eta.data_ptr(), tt.data_ptr() if terms else 0, coi, st.cuda_stream)
+        return (eta, tt) if terms else eta
+
+    def region_partials(self, regions):
+        """[(kappa, k1, k2), ...] -> array [n, 6]: D_w, E_w, F_w, G_w, H_w, n_points (last call)."""
+        r = np.asarray(regions, dtype=np.int32).reshape(-1, 3)
+        k, a, b = (np.ascontiguousarray(r[:, i]) for i in range(3))
+        out = np.zeros((len(r), 6))
+        _abi.check(_abi.lib.isrs_egn_region_partials(
+            self._h, len(r), k.ctypes.data_as(_abi._ip), a.ctypes.data_as(_abi._ip),
+            b.ctypes.data_as(_abi._ip), out.ctypes.data_as(_abi._dp)))
+        return out
+
+    def work(self):
+        """(points, point_spans, regions) of the last nli call."""
+        p, ps, r = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _abi.check(_abi.lib.isrs_egn_work(self._h, ctypes.byref(p), ctypes.byref(ps), ctypes.byref(r)))
+        return p.value, ps.value, r.value
+
+    def last_launch_count(self):
+        return _abi.lib.isrs_egn_last_launch_count(self._h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _abi.lib.isrs_egn_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def eta_host(link, coi=None, grid_n=None, delta_z_m=None, device=0, precision=64, mu_mode=MU_SEGMENT,
+             flags=0, terms=False):
+    """One-shot end-to-end call with host buffers (isrs_egn_eta_host)."""
+    pa = ProblemArrays(link)
+    n = numerics(grid_n if grid_n is not None else link.grid_n,
+                 delta_z_m if delta_z_m is not None else getattr(link, "delta_z_m", 1000.0),
+                 precision, mu_mode, flags)
+    if coi is None:
+        nco, cp = pa.struct.n_ch, None
+    else:
+        c = np.ascontiguousarray(np.asarray(coi, dtype=np.int32))
+        nco, cp = len(c), c.ctypes.data_as(_abi._ip)
+    eta = np.zeros(nco)
+    tt = np.zeros((nco, 5)) if terms else None
+    _abi.check(_abi.lib.isrs_egn_eta_host(ctypes.byref(pa.struct), ctypes.byref(n), device, nco, cp,
+                                          eta.ctypes.data_as(_abi._dp),
+                                          tt.ctypes.data_as(_abi._dp) if terms else _abi._dp()))
+    return (eta, tt) if terms else eta

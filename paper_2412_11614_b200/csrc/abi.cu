@@ -1,0 +1,461 @@
+// C ABI + host planner (rows a1 and b) of the ISRS EGN hot path.  See include/isrs_egn.h.
+//
+// Planner (row a1): validation, canonicalisation (reading C5: offsets from the occupied-band
+// midpoint f_c, B_tot edge-to-edge, P_tot = sum P_i; K_s = ceil(L_s/dz)), span classes
+// (spans with equal L, alpha, C_r share envelope tables), the region work list of every COI
+// (Eq. 16, generalised to arbitrary channel plans: a region (kappa, k1, k2) is listed
+// when the f3 range of its bin centres overlaps some band) split into D-only and coherent
+// (E/F/G/H-carrying, reading C8) lists.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/isrs_egn.h"
+#include "internal.h"
+
+using namespace isrs;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  ~DevBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  bool alloc(size_t count) {
+    reset();
+    if (count == 0) count = 1;
+    if (cudaMalloc(&p, count * sizeof(T)) != cudaSuccess) {
+      p = nullptr;
+      return false;
+    }
+    n = count;
+    return true;
+  }
+  bool upload(const std::vector<T>& v) {
+    if (!alloc(v.size())) return false;
+    if (v.empty()) return true;
+    return cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice) == cudaSuccess;
+  }
+};
+
+struct WorkList {
+  std::vector<int> coi;
+  std::vector<RegionDesc> desc;
+  std::vector<long long> coi_off;
+  std::vector<int> list_d, list_c;
+};
+
+}  // namespace
+
+struct isrs_egn {
+  int device = 0;
+  isrs_egn_numerics num{};
+  int n_ch = 0, n_span = 0, n_cls = 0, N = 0;
+  // host canonical data
+  std::vector<double> lo, hi, f, G, R, P, phi, psi, delta;
+  std::vector<long long> rate;
+  double f_c = 0, b_tot = 0, p_tot = 0;
+  // device data
+  DevBuf<double> d_lo, d_hi, d_f, d_G, d_R, d_P, d_phi, d_psi, d_delta;
+  DevBuf<long long> d_rate;
+  DevBuf<double> d_A2, d_A3, d_Eh, d_ah, d_gh, d_macc, d_aL;
+  DevBuf<int> d_K, d_cls, d_Kc;
+  DevBuf<double> d_lnA, d_zeta;
+  int kstride = 0, tstride = 0, tw = 0;
+  // work list cache (last call)
+  WorkList wl;
+  bool wl_all = false;
+  DevBuf<RegionDesc> d_desc;
+  DevBuf<long long> d_coi_off;
+  DevBuf<int> d_coi, d_list_d, d_list_c;
+  DevBuf<double> d_partials, d_npts;
+  cudaStream_t last_stream = nullptr;
+  bool have_result = false;
+  int last_launches = 0;
+};
+
+static bool is_fin(double x) { return std::isfinite(x); }
+
+static int validate(const isrs_egn_problem* p, const isrs_egn_numerics* n) {
+  if (!p || !n) return fail(ISRS_EGN_EINVAL, "problem/numerics is NULL");
+  if (p->n_ch < 1) return fail(ISRS_EGN_EINVAL, "n_ch < 1");
+  if (p->n_span < 1) return fail(ISRS_EGN_EINVAL, "n_span < 1");
+  if (!p->f_center_hz || !p->symbol_rate_hz || !p->launch_power_w || !p->excess_kurtosis)
+    return fail(ISRS_EGN_EINVAL, "channel array is NULL");
+  if (!p->length_m || !p->alpha_per_m || !p->beta2_s2_per_m || !p->beta3_s3_per_m ||
+      !p->gamma_per_w_m || !p->cr_per_w_m_hz)
+    return fail(ISRS_EGN_EINVAL, "span array is NULL");
+  if (n->grid_n < 2 || (n->grid_n & 1)) return fail(ISRS_EGN_EINVAL, "grid_n must be even and >= 2");
+  if (n->grid_n > 4096) return fail(ISRS_EGN_EINVAL, "grid_n > 4096");
+  if (!is_fin(n->delta_z_m) || n->delta_z_m <= 0) return fail(ISRS_EGN_EINVAL, "delta_z_m <= 0");
+  if (n->precision != 64 && n->precision != 32 && n->precision != 0)
+    return fail(ISRS_EGN_EUNSUPPORTED, "precision must be 64 or 32");
+  if (n->precision == 32) return fail(ISRS_EGN_EUNSUPPORTED, "fp32 variant not built in this version");
+  if (n->mu_mode != ISRS_EGN_MU_SEGMENT && n->mu_mode != ISRS_EGN_MU_MACLAURIN)
+    return fail(ISRS_EGN_EUNSUPPORTED, "unknown mu_mode");
+  const double lim = 4.0e15;  // |values| < 2^52: integer-Hz arithmetic exact
+  for (int i = 0; i < p->n_ch; ++i) {
+    const double F = p->f_center_hz[i], R = p->symbol_rate_hz[i], P = p->launch_power_w[i];
+    const std::string at = "[" + std::to_string(i) + "]";
+    if (!is_fin(F) || F <= 0 || F > lim || F != std::floor(F))
+      return fail(ISRS_EGN_EINVAL, "f_center_hz" + at + " must be a positive integer number of Hz");
+    if (!is_fin(R) || R <= 0 || R > 1e14 || R != std::floor(R))
+      return fail(ISRS_EGN_EINVAL, "symbol_rate_hz" + at + " must be a positive integer number of Hz");
+    const double half = R / (2.0 * n->grid_n);
+    if (half != std::floor(half))
+      return fail(ISRS_EGN_EINVAL, "symbol_rate_hz" + at + " / (2 grid_n) must be an integer (C10)");
+    if (!is_fin(P) || P <= 0) return fail(ISRS_EGN_EINVAL, "launch_power_w" + at + " must be > 0");
+    if (!is_fin(p->excess_kurtosis[i])) return fail(ISRS_EGN_EINVAL, "excess_kurtosis" + at);
+    if (p->psi && !is_fin(p->psi[i])) return fail(ISRS_EGN_EINVAL, "psi" + at);
+    if (i > 0 && !(F > p->f_center_hz[i - 1]))
+      return fail(ISRS_EGN_EINVAL, "f_center_hz" + at + " not strictly increasing");
+    if (i > 0 && F - R / 2 < p->f_center_hz[i - 1] + p->symbol_rate_hz[i - 1] / 2)
+      return fail(ISRS_EGN_EOVERLAP, "bands of channels " + std::to_string(i - 1) + " and " +
+                                         std::to_string(i) + " overlap");
+  }
+  for (int s = 0; s < p->n_span; ++s) {
+    const std::string at = "[" + std::to_string(s) + "]";
+    if (!is_fin(p->length_m[s]) || p->length_m[s] <= 0) return fail(ISRS_EGN_EINVAL, "length_m" + at + " <= 0");
+    if (!is_fin(p->alpha_per_m[s]) || p->alpha_per_m[s] <= 0)
+      return fail(ISRS_EGN_EINVAL, "alpha_per_m" + at + " must be > 0 (Eq. 9 divides by i chi - alpha)");
+    if (!is_fin(p->beta2_s2_per_m[s])) return fail(ISRS_EGN_EINVAL, "beta2_s2_per_m" + at);
+    if (!is_fin(p->beta3_s3_per_m[s])) return fail(ISRS_EGN_EINVAL, "beta3_s3_per_m" + at);
+    if (!is_fin(p->gamma_per_w_m[s]) || p->gamma_per_w_m[s] < 0) return fail(ISRS_EGN_EINVAL, "gamma_per_w_m" + at + " < 0");
+    if (!is_fin(p->cr_per_w_m_hz[s]) || p->cr_per_w_m_hz[s] < 0) return fail(ISRS_EGN_EINVAL, "cr_per_w_m_hz" + at + " < 0");
+    const double K = std::ceil(p->length_m[s] / n->delta_z_m);
+    if (K > (1 << 20)) return fail(ISRS_EGN_ERANGE, "K_s = ceil(L/dz) > 2^20 for span" + at);
+  }
+  return ISRS_EGN_OK;
+}
+
+static int cuda_fail(cudaError_t e, const char* what) {
+  return fail(ISRS_EGN_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numerics* n, int device,
+                               isrs_egn_t** out) {
+  if (!out) return fail(ISRS_EGN_EINVAL, "out is NULL");
+  *out = nullptr;
+  isrs_egn_numerics num = n ? *n : isrs_egn_numerics{};
+  if (num.precision == 0) num.precision = 64;
+  int rc = validate(p, &num);
+  if (rc) return rc;
+  cudaError_t ce = cudaSetDevice(device);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaSetDevice");
+
+  auto* h = new isrs_egn();
+  h->device = device;
+  h->num = num;
+  h->n_ch = p->n_ch;
+  h->n_span = p->n_span;
+  h->N = num.grid_n;
+  const int nc = p->n_ch, N = num.grid_n;
+  // ---- canonicalisation (reading C5)
+  double lo_min = 1e300, hi_max = -1e300;
+  for (int i = 0; i < nc; ++i) {
+    lo_min = std::min(lo_min, p->f_center_hz[i] - p->symbol_rate_hz[i] / 2);
+    hi_max = std::max(hi_max, p->f_center_hz[i] + p->symbol_rate_hz[i] / 2);
+  }
+  h->f_c = (lo_min + hi_max) / 2;
+  h->b_tot = hi_max - lo_min;
+  h->p_tot = 0;
+  for (int i = 0; i < nc; ++i) {
+    const double F = p->f_center_hz[i] - h->f_c, R = p->symbol_rate_hz[i];
+    h->f.push_back(F);
+    h->R.push_back(R);
+    h->lo.push_back(F - R / 2);
+    h->hi.push_back(F + R / 2);
+    h->P.push_back(p->launch_power_w[i]);
+    h->G.push_back(p->launch_power_w[i] / R);
+    h->phi.push_back(p->excess_kurtosis[i]);
+    h->psi.push_back(p->psi ? p->psi[i] : 0.0);
+    h->delta.push_back(R / N);
+    h->rate.push_back((long long)R);
+    h->p_tot += p->launch_power_w[i];
+  }
+  // ---- spans and classes
+  std::map<std::tuple<double, double, double>, int> cls_of;
+  std::vector<double> cL, cA, cC;
+  std::vector<int> cK;
+  std::vector<double> A2, A3, Eh, ah, gh, macc, aL;
+  std::vector<int> K, cls;
+  for (int s = 0; s < p->n_span; ++s) {
+    const double L = p->length_m[s], a = p->alpha_per_m[s], cr = p->cr_per_w_m_hz[s];
+    const int Ks = (int)std::ceil(L / num.delta_z_m);
+    const double hs = L / Ks;
+    auto key = std::make_tuple(L, a, cr);
+    auto it = cls_of.find(key);
+    int c;
+    if (it == cls_of.end()) {
+      c = (int)cL.size();
+      cls_of[key] = c;
+      cL.push_back(L);
+      cA.push_back(a);
+      cC.push_back(cr);
+      cK.push_back(Ks);
+      const double x = h->b_tot * h->p_tot * cr * (-std::expm1(-a * L) / a);
+      if (x > 1400.0) {
+        delete h;
+        return fail(ISRS_EGN_ERANGE, "B_tot P_tot C_r L_eff too large (sinh overflow) for span " +
+                                         std::to_string(s));
+      }
+    } else {
+      c = it->second;
+    }
+    cls.push_back(c);
+    K.push_back(Ks);
+    A2.push_back(4.0 * M_PI * p->beta2_s2_per_m[s] * hs);
+    A3.push_back(4.0 * M_PI * M_PI * p->beta3_s3_per_m[s] * hs);
+    Eh.push_back(std::exp(-a * hs));
+    ah.push_back(a * hs);
+    gh.push_back(p->gamma_per_w_m[s] * hs);
+    macc.push_back(h->p_tot * cr / a);
+    aL.push_back(a * L);
+  }
+  h->n_cls = (int)cL.size();
+  int kmax = *std::max_element(cK.begin(), cK.end());
+  int kpad = (kmax + 1) & ~1;
+  h->kstride = kpad;
+  h->tstride = kpad + 2;
+  const size_t t_budget = 48 * 1024;
+  h->tw = (int)std::min<size_t>(TW_MAX, t_budget / ((size_t)h->tstride * 8));
+  if (h->tw < 2) {
+    delete h;
+    return fail(ISRS_EGN_ERANGE, "K_s too large for the shared-memory envelope table (reduce K or raise dz)");
+  }
+  const size_t smem = integrand_smem_bytes(h->tstride, h->tw, N, true);
+  if (smem > 220 * 1024) {
+    delete h;
+    return fail(ISRS_EGN_ERANGE, "grid_n / K_s exceed the shared-memory budget");
+  }
+  bool ok = h->d_lo.upload(h->lo) && h->d_hi.upload(h->hi) && h->d_f.upload(h->f) &&
+            h->d_G.upload(h->G) && h->d_R.upload(h->R) && h->d_P.upload(h->P) &&
+            h->d_phi.upload(h->phi) && h->d_psi.upload(h->psi) && h->d_delta.upload(h->delta) &&
+            h->d_rate.upload(h->rate) && h->d_A2.upload(A2) && h->d_A3.upload(A3) &&
+            h->d_Eh.upload(Eh) && h->d_ah.upload(ah) && h->d_gh.upload(gh) &&
+            h->d_macc.upload(macc) && h->d_aL.upload(aL) && h->d_K.upload(K) && h->d_cls.upload(cls) &&
+            h->d_Kc.upload(cK);
+  DevBuf<double> dL, dA, dC;
+  ok = ok && dL.upload(cL) && dA.upload(cA) && dC.upload(cC) &&
+       h->d_lnA.alloc((size_t)h->n_cls * h->kstride) && h->d_zeta.alloc((size_t)h->n_cls * h->kstride);
+  if (!ok) {
+    delete h;
+    return fail(ISRS_EGN_ENOMEM, "device allocation/upload failed");
+  }
+  PParams pp{dL.p, dA.p, dC.p, h->d_Kc.p, h->n_cls, h->kstride, h->p_tot, h->b_tot, h->d_lnA.p, h->d_zeta.p};
+  if (launch_precompute(pp, nullptr) != 0) {
+    delete h;
+    return cuda_fail(cudaGetLastError(), "precompute launch");
+  }
+  ce = cudaDeviceSynchronize();
+  if (ce != cudaSuccess) {
+    delete h;
+    return cuda_fail(ce, "precompute");
+  }
+  *out = h;
+  return ISRS_EGN_OK;
+}
+
+// Region enumeration for the given COIs (canonical order: COI, then k1, then k2).
+static void build_worklist(const isrs_egn* h, const std::vector<int>& coi, WorkList* w) {
+  w->coi = coi;
+  w->desc.clear();
+  w->coi_off.assign(1, 0);
+  w->list_d.clear();
+  w->list_c.clear();
+  const int nc = h->n_ch;
+  for (int kappa : coi) {
+    const double f = h->f[kappa];
+    for (int k1 = 0; k1 < nc; ++k1) {
+      for (int k2 = 0; k2 < nc; ++k2) {
+        const double lo3 = h->lo[k1] + h->lo[k2] - f + (h->delta[k1] + h->delta[k2]) / 2;
+        const double hi3 = h->hi[k1] + h->hi[k2] - f - (h->delta[k1] + h->delta[k2]) / 2;
+        // first band with hi >= lo3
+        int i = (int)(std::lower_bound(h->hi.begin(), h->hi.end(), lo3) - h->hi.begin());
+        if (i >= nc || h->lo[i] > hi3) continue;
+        auto overlaps = [&](int c) { return h->hi[c] >= lo3 && h->lo[c] <= hi3; };
+        int flags = 0;
+        if (h->phi[k1] != 0.0 && overlaps(k1)) flags |= NEED_E;
+        if (h->phi[k2] != 0.0 && overlaps(k2)) flags |= NEED_F;
+        if (h->phi[k1] != 0.0 && k1 == k2) flags |= NEED_G;
+        if (h->psi[k1] != 0.0 && k1 == k2 && overlaps(k1)) flags |= NEED_H;
+        if (h->num.flags & ISRS_EGN_FLAG_UNIT_LINK) {
+          // unit link hook: same gating
+        }
+        const int id = (int)w->desc.size();
+        w->desc.push_back(RegionDesc{kappa, k1, k2, flags});
+        (flags ? w->list_c : w->list_d).push_back(id);
+      }
+    }
+    w->coi_off.push_back((long long)w->desc.size());
+  }
+}
+
+extern "C" int isrs_egn_nli(isrs_egn_t* h, int32_t n_coi, const int32_t* coi, double* eta_dev,
+                            double* terms_dev, void* cuda_stream) {
+  if (!h) return fail(ISRS_EGN_EINVAL, "handle is NULL");
+  if (!eta_dev) return fail(ISRS_EGN_EINVAL, "eta_dev is NULL");
+  std::vector<int> c;
+  if (!coi) {
+    if (n_coi != h->n_ch) return fail(ISRS_EGN_EINVAL, "coi == NULL requires n_coi == n_ch");
+    for (int i = 0; i < h->n_ch; ++i) c.push_back(i);
+  } else {
+    if (n_coi < 1) return fail(ISRS_EGN_EINVAL, "n_coi < 1");
+    for (int i = 0; i < n_coi; ++i) {
+      if (coi[i] < 0 || coi[i] >= h->n_ch)
+        return fail(ISRS_EGN_EINVAL, "coi[" + std::to_string(i) + "] out of range");
+      c.push_back(coi[i]);
+    }
+  }
+  cudaError_t ce = cudaSetDevice(h->device);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaSetDevice");
+  ce = cudaGetLastError();
+  if (ce != cudaSuccess) return cuda_fail(ce, "pending CUDA error");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  if (!(h->have_result || h->wl.desc.size()) || h->wl.coi != c) {
+    // (re)build and upload the work list for this COI set (cached across identical calls)
+    cudaStreamSynchronize(h->last_stream);
+    build_worklist(h, c, &h->wl);
+    bool ok = h->d_desc.upload(h->wl.desc) && h->d_coi_off.upload(h->wl.coi_off) &&
+              h->d_coi.upload(h->wl.coi) && h->d_list_d.upload(h->wl.list_d) &&
+              h->d_list_c.upload(h->wl.list_c) && h->d_partials.alloc(h->wl.desc.size() * 6) &&
+              h->d_npts.alloc(c.size());
+    if (!ok) return fail(ISRS_EGN_ENOMEM, "work-list allocation failed");
+  }
+  KParams kp{};
+  kp.lo = h->d_lo.p; kp.hi = h->d_hi.p; kp.f = h->d_f.p; kp.G = h->d_G.p; kp.R = h->d_R.p;
+  kp.P = h->d_P.p; kp.phi = h->d_phi.p; kp.psi = h->d_psi.p; kp.delta = h->d_delta.p;
+  kp.rate = h->d_rate.p; kp.n_ch = h->n_ch;
+  kp.A2 = h->d_A2.p; kp.A3 = h->d_A3.p; kp.Eh = h->d_Eh.p; kp.ah = h->d_ah.p; kp.gh = h->d_gh.p;
+  kp.mac_c = h->d_macc.p; kp.aL = h->d_aL.p; kp.K = h->d_K.p; kp.cls = h->d_cls.p;
+  kp.n_span = h->n_span;
+  kp.lnA = h->d_lnA.p; kp.zeta = h->d_zeta.p; kp.Kc = h->d_Kc.p; kp.n_cls = h->n_cls;
+  kp.kstride = h->kstride; kp.tstride = h->tstride; kp.tw = h->tw; kp.N = h->N;
+  kp.desc = h->d_desc.p; kp.partials = h->d_partials.p;
+  kp.mode = (h->num.flags & ISRS_EGN_FLAG_UNIT_LINK) ? MODE_UNIT
+            : (h->num.mu_mode == ISRS_EGN_MU_MACLAURIN ? MODE_MACLAURIN : MODE_SEGMENT);
+  int launches = 0;
+  if (launch_integrand(kp, h->d_list_d.p, (long long)h->wl.list_d.size(), false, st, &launches) != 0)
+    return cuda_fail(cudaGetLastError(), "integrand launch (D-only regions)");
+  if (launch_integrand(kp, h->d_list_c.p, (long long)h->wl.list_c.size(), true, st, &launches) != 0)
+    return cuda_fail(cudaGetLastError(), "integrand launch (coherent regions)");
+  RParams rp{h->d_desc.p, h->d_partials.p, h->d_coi_off.p, h->d_coi.p, h->d_G.p, h->d_R.p,
+             h->d_P.p, h->d_phi.p, h->d_psi.p, (int)c.size(), eta_dev, terms_dev, h->d_npts.p};
+  if (launch_reduce(rp, st) != 0) return cuda_fail(cudaGetLastError(), "reduce launch");
+  launches += 1;
+  h->last_launches = launches;
+  h->last_stream = st;
+  h->have_result = true;
+  return ISRS_EGN_OK;
+}
+
+extern "C" int isrs_egn_region_partials(isrs_egn_t* h, int32_t n, const int32_t* kappa,
+                                        const int32_t* k1, const int32_t* k2, double* out_host) {
+  if (!h || !out_host || n < 0 || (n > 0 && (!kappa || !k1 || !k2)))
+    return fail(ISRS_EGN_EINVAL, "bad argument");
+  if (!h->have_result) return fail(ISRS_EGN_EINVAL, "no isrs_egn_nli() result yet");
+  cudaError_t ce = cudaStreamSynchronize(h->last_stream);
+  if (ce != cudaSuccess) return cuda_fail(ce, "stream sync");
+  const auto& w = h->wl;
+  for (int q = 0; q < n; ++q) {
+    double* o = out_host + 6 * (size_t)q;
+    for (int k = 0; k < 5; ++k) o[k] = 0.0;
+    o[5] = -1.0;
+    auto itc = std::find(w.coi.begin(), w.coi.end(), kappa[q]);
+    if (itc == w.coi.end()) continue;
+    const size_t ci = itc - w.coi.begin();
+    for (long long r = w.coi_off[ci]; r < w.coi_off[ci + 1]; ++r) {
+      if (w.desc[r].k1 == k1[q] && w.desc[r].k2 == k2[q]) {
+        ce = cudaMemcpy(o, h->d_partials.p + r * 6, 6 * sizeof(double), cudaMemcpyDeviceToHost);
+        if (ce != cudaSuccess) return cuda_fail(ce, "partials copy");
+        break;
+      }
+    }
+  }
+  return ISRS_EGN_OK;
+}
+
+extern "C" int isrs_egn_work(isrs_egn_t* h, int64_t* points, int64_t* point_spans, int64_t* regions) {
+  if (!h) return fail(ISRS_EGN_EINVAL, "handle is NULL");
+  if (!h->have_result) return fail(ISRS_EGN_EINVAL, "no isrs_egn_nli() result yet");
+  cudaError_t ce = cudaStreamSynchronize(h->last_stream);
+  if (ce != cudaSuccess) return cuda_fail(ce, "stream sync");
+  std::vector<double> np(h->wl.coi.size());
+  ce = cudaMemcpy(np.data(), h->d_npts.p, np.size() * sizeof(double), cudaMemcpyDeviceToHost);
+  if (ce != cudaSuccess) return cuda_fail(ce, "npts copy");
+  long long tot = 0;
+  for (double v : np) tot += (long long)v;
+  if (points) *points = tot;
+  if (point_spans) *point_spans = tot * h->n_span;
+  if (regions) *regions = (long long)h->wl.desc.size();
+  return ISRS_EGN_OK;
+}
+
+extern "C" int isrs_egn_last_launch_count(const isrs_egn_t* h) { return h ? h->last_launches : 0; }
+
+extern "C" int isrs_egn_eta_host(const isrs_egn_problem* p, const isrs_egn_numerics* n, int device,
+                                 int32_t n_coi, const int32_t* coi, double* eta_host, double* terms_host) {
+  if (!eta_host) return fail(ISRS_EGN_EINVAL, "eta_host is NULL");
+  isrs_egn_t* h = nullptr;
+  int rc = isrs_egn_create(p, n, device, &h);
+  if (rc) return rc;
+  const int nco = coi ? n_coi : p->n_ch;
+  double* d = nullptr;
+  cudaError_t ce = cudaMalloc(&d, sizeof(double) * (size_t)nco * 6);
+  if (ce != cudaSuccess) {
+    isrs_egn_destroy(h);
+    return cuda_fail(ce, "cudaMalloc");
+  }
+  rc = isrs_egn_nli(h, nco, coi, d, terms_host ? d + nco : nullptr, nullptr);
+  if (rc == 0) {
+    ce = cudaMemcpy(eta_host, d, sizeof(double) * nco, cudaMemcpyDeviceToHost);
+    if (ce == cudaSuccess && terms_host)
+      ce = cudaMemcpy(terms_host, d + nco, sizeof(double) * nco * 5, cudaMemcpyDeviceToHost);
+    if (ce != cudaSuccess) rc = cuda_fail(ce, "result copy");
+  }
+  cudaFree(d);
+  isrs_egn_destroy(h);
+  return rc;
+}
+
+extern "C" void isrs_egn_destroy(isrs_egn_t* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  delete h;
+}
+
+extern "C" const char* isrs_egn_strerror(int code) {
+  switch (code) {
+    case ISRS_EGN_OK: return "ok";
+    case ISRS_EGN_EINVAL: return "invalid argument";
+    case ISRS_EGN_EOVERLAP: return "channel bands overlap";
+    case ISRS_EGN_ERANGE: return "value out of supported range";
+    case ISRS_EGN_ENOMEM: return "out of memory";
+    case ISRS_EGN_ECUDA: return "CUDA error";
+    case ISRS_EGN_EUNSUPPORTED: return "unsupported option";
+    default: return "unknown status";
+  }
+}
+
+extern "C" const char* isrs_egn_last_error(void) { return g_err.c_str(); }

@@ -1,0 +1,98 @@
+// Internal device-side data layout shared by the host planner (abi.cu) and the kernels
+// (kernels.cu).  Not part of the public ABI (include/isrs_egn.h is).
+#pragma once
+#include <cstdint>
+
+namespace isrs {
+
+constexpr int BLOCK = 256;          // threads per CTA (8 warps)
+constexpr int PPT = 4;              // grid points per thread in flight (independent Goertzel chains)
+constexpr int CP = BLOCK * PPT;     // points per chunk
+constexpr int LINE_CAP = 512;       // f3-lines compacted per segment (2N-1 <= 511 at N = 256)
+constexpr int TW_MAX = 64;          // envelope-table rows (f3-lines) resident in smem
+
+// region flags (reading C8: a term whose gate or weight is zero is not evaluated)
+enum : int { NEED_E = 1, NEED_F = 2, NEED_G = 4, NEED_H = 8 };
+
+enum : int { MODE_SEGMENT = 0, MODE_MACLAURIN = 1, MODE_UNIT = 2 };
+
+struct RegionDesc {
+  int kappa, k1, k2, flags;
+};
+
+// Everything a kernel needs, passed by value (all pointers are device pointers).
+struct KParams {
+  // channels (offset frequencies from f_c, exact multiples of 1/2 Hz)
+  const double* lo;
+  const double* hi;
+  const double* f;
+  const double* G;      // PSD P/R
+  const double* R;
+  const double* P;
+  const double* phi;
+  const double* psi;
+  const double* delta;  // R/N
+  const long long* rate;  // R as integer Hz (for the lattice ratio a:b)
+  int n_ch;
+  // spans
+  const double* A2;     // 4 pi beta2 h        (chi h / pi = u v (A2 + A3 (f1+f2)))
+  const double* A3;     // 4 pi^2 beta3 h
+  const double* Eh;     // e^{-alpha h}
+  const double* ah;     // alpha h
+  const double* gh;     // gamma h
+  const double* mac_c;  // Maclaurin: P_tot C_r / alpha
+  const double* aL;     // alpha L
+  const int* K;         // segments K_s = ceil(L/dz)
+  const int* cls;       // span class (spans sharing L, alpha, C_r share envelope tables)
+  int n_span;
+  // span classes: envelope a'_k(f3) = exp(lnA[c][k] - zeta[c][k] f3)
+  const double* lnA;    // [n_cls][kstride]  ln(c_k) - alpha h k
+  const double* zeta;   // [n_cls][kstride]
+  const int* Kc;        // [n_cls]
+  int n_cls;
+  int kstride;          // row length of lnA/zeta
+  int tstride;          // smem table row stride (even, = Kpad + 2)
+  int tw;               // table rows resident (<= TW_MAX)
+  int N;                // grid points per channel axis
+  // regions
+  const RegionDesc* desc;
+  double* partials;     // [n_regions][6]: D_w, E_w, F_w, G_w, H_w, n_points
+  int mode;
+};
+
+struct RParams {
+  const RegionDesc* desc;
+  const double* partials;
+  const long long* coi_off;  // [n_coi + 1] region ranges per COI (canonical order)
+  const int* coi;            // [n_coi]
+  const double* G;
+  const double* R;
+  const double* P;
+  const double* phi;
+  const double* psi;
+  int n_coi;
+  double* eta;
+  double* terms;             // may be null
+  double* npts;              // [n_coi]
+};
+
+struct PParams {  // precompute
+  const double* cls_L;
+  const double* cls_alpha;
+  const double* cls_cr;
+  const int* Kc;
+  int n_cls;
+  int kstride;
+  double p_tot;
+  double b_tot;
+  double* lnA;
+  double* zeta;
+};
+
+size_t integrand_smem_bytes(int tstride, int tw, int N, bool coherent);
+int launch_precompute(const PParams& p, void* stream);
+int launch_integrand(const KParams& p, const int* list, long long n_list, bool coherent,
+                     void* stream, int* n_launches);
+int launch_reduce(const RParams& p, void* stream);
+
+}  // namespace isrs

@@ -1,0 +1,648 @@
+// sm_100a kernels of the ISRS EGN hot path (paper arXiv 2412.11614).
+//
+//   precompute_kernel  (row a2)  per span class c and segment k: zeta_k = P_tot C_r L_eff(z_k)
+//                                 (Eq. 2; z_k Eq. 10) and the SRS-gain normalisation
+//                                 c_k = x / (2 sinh(x/2)), x = B_tot zeta_k (Eq. 14), stored
+//                                 as lnA = ln c_k - alpha h k  (the attenuation factor folded in).
+//   integrand_kernel   (rows a3-a6) one CTA per region (kappa, kappa1, kappa2): f3-gate per line
+//                                 (Eq. 17 gate, reading C10), the segment closed form mu_s (Eqs. 8-9,
+//                                 P:119-121) for every point and span, the span phased-array sum Y
+//                                 (Eq. 22, reading C3) in registers, and the D, E, F, G, H
+//                                 region reductions (Eqs. 17-21, reading C7), fixed order.
+//   reduce_kernel      (row a7)  per COI: Eq. 15 coefficients (reading C2) and Eq. 11.
+//
+// FP64 CUDA-core work (no tensor cores: the path is not a dense contraction).  The segment sum
+//   mu_s = I_0 * sum_k a_k w^k,  w = e^{(i chi - alpha) h},  I_0 = (w - 1)/(i chi - alpha)
+// (Eq. 9 gives I_k = I_0 w^k) has REAL coefficients a_k = c_k e^{-zeta_k f3}; with the attenuation
+// folded in (a'_k = a_k e^{-alpha h k}, z = e^{i chi h}, |z| = 1) it is evaluated by the
+// second-order real recurrence b_k = a'_k + 2 cos(chi h) b_{k+1} - b_{k+2} (Goertzel), i.e.
+// ONE DFMA + ONE DADD per segment instead of a complex Horner step (4 DP instructions).
+// Envelope values a'_k(f3) depend on the point only through f3, which is constant along the
+// lattice lines j = a m1 + b m2 of a region (a:b = R1:R2), so they are tabulated per line in
+// shared memory and read with 16-byte loads that a warp mostly broadcasts.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+
+#include "internal.h"
+
+namespace isrs {
+
+// ------------------------------------------------------------------------------------------
+// precompute (row a2)
+
+__global__ void precompute_kernel(const PParams p) {
+  const int c = blockIdx.y;
+  const int K = p.Kc[c];
+  const double L = p.cls_L[c], alpha = p.cls_alpha[c], cr = p.cls_cr[c];
+  const double h = L / K;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < p.kstride; k += gridDim.x * blockDim.x) {
+    double lnA = 0.0, ze = 0.0;
+    if (k < K) {
+      const double zk = (k + 0.5) * h;                    // Eq. 10
+      const double leff = -expm1(-alpha * zk) / alpha;     // L_eff(z_k)
+      ze = p.p_tot * cr * leff;                            // Eq. 2: zeta = P_tot C_r L_eff
+      const double x = p.b_tot * ze;
+      const double ck = (x == 0.0) ? 1.0 : x / (2.0 * sinh(0.5 * x));  // Eq. 14 normalisation
+      lnA = log(ck) - alpha * h * k;                       // attenuation |w|^k folded in
+    }
+    p.lnA[(size_t)c * p.kstride + k] = lnA;
+    p.zeta[(size_t)c * p.kstride + k] = ze;
+  }
+}
+
+int launch_precompute(const PParams& p, void* stream) {
+  dim3 grid((p.kstride + 127) / 128, p.n_cls);
+  precompute_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(p);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+// ------------------------------------------------------------------------------------------
+// integrand helpers
+
+struct Smem {
+  double* T;         // [tw][tstride] reversed envelope rows: T[row][i] = a'_{Kp-1-i}(f3_row)
+  int* sl_j;         // [LINE_CAP] compacted supported line index j
+  int* sl_first;     // [LINE_CAP] first m1 on the line
+  int* sl_start;     // [LINE_CAP+1] exclusive prefix of point counts
+  double* wD;        // [LINE_CAP] sum_t t G_k3         (D, G weights)
+  double* wE;        // [LINE_CAP] sum_t t [k3 == k1]   (E, H weights)
+  int* scan;         // [BLOCK] scan scratch (int2)
+  double* red;       // [BLOCK] reduction scratch
+  double2* ybuf;     // [CP] chunk Y values (coherent only)
+  double2* rowacc;   // [N]
+  double2* colacc;   // [N]
+  double2* lineacc;  // [LINE_CAP]
+  double* wF;        // [LINE_CAP] sum_t t [k3 == k2]
+};
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+__host__ __device__ inline size_t smem_layout(int tstride, int tw, int N, bool coh, char* base,
+                                              Smem* s) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align16(off + bytes);
+    return o;
+  };
+  size_t oT = take(sizeof(double) * (size_t)tw * tstride);
+  size_t oJ = take(sizeof(int) * LINE_CAP);
+  size_t oF = take(sizeof(int) * LINE_CAP);
+  size_t oS = take(sizeof(int) * (LINE_CAP + 1));
+  size_t oD = take(sizeof(double) * LINE_CAP);
+  size_t oE = take(sizeof(double) * LINE_CAP);
+  size_t oW = take(sizeof(double) * LINE_CAP);
+  size_t oC = take(sizeof(int) * 2 * BLOCK);
+  size_t oR = take(sizeof(double) * BLOCK);
+  size_t oY = 0, oRow = 0, oCol = 0, oLine = 0;
+  if (coh) {
+    oY = take(sizeof(double2) * CP);
+    oRow = take(sizeof(double2) * N);
+    oCol = take(sizeof(double2) * N);
+    oLine = take(sizeof(double2) * LINE_CAP);
+  }
+  if (s) {
+    s->T = (double*)(base + oT);
+    s->sl_j = (int*)(base + oJ);
+    s->sl_first = (int*)(base + oF);
+    s->sl_start = (int*)(base + oS);
+    s->wD = (double*)(base + oD);
+    s->wE = (double*)(base + oE);
+    s->wF = (double*)(base + oW);
+    s->scan = (int*)(base + oC);
+    s->red = (double*)(base + oR);
+    s->ybuf = coh ? (double2*)(base + oY) : nullptr;
+    s->rowacc = coh ? (double2*)(base + oRow) : nullptr;
+    s->colacc = coh ? (double2*)(base + oCol) : nullptr;
+    s->lineacc = coh ? (double2*)(base + oLine) : nullptr;
+  }
+  return off;
+}
+
+size_t integrand_smem_bytes(int tstride, int tw, int N, bool coherent) {
+  return smem_layout(tstride, tw, N, coherent, nullptr, nullptr);
+}
+
+// Block-wide exclusive scan of an int pair; returns totals.  All threads must call.
+__device__ inline int2 block_scan2(int2 v, int* scratch, int2* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int2 x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int a = __shfl_up_sync(0xffffffffu, x.x, o);
+    int b = __shfl_up_sync(0xffffffffu, x.y, o);
+    if (lane >= o) { x.x += a; x.y += b; }
+  }
+  int2* ws = (int2*)scratch;
+  __syncthreads();
+  if (lane == 31) ws[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int2 w = (lane < BLOCK / 32) ? ws[lane] : make_int2(0, 0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int a = __shfl_up_sync(0xffffffffu, w.x, o);
+      int b = __shfl_up_sync(0xffffffffu, w.y, o);
+      if (lane >= o) { w.x += a; w.y += b; }
+    }
+    if (lane < BLOCK / 32) ws[lane] = w;   // inclusive warp prefix
+  }
+  __syncthreads();
+  int2 base = (warp > 0) ? ws[warp - 1] : make_int2(0, 0);
+  *total = ws[BLOCK / 32 - 1];
+  __syncthreads();
+  return make_int2(base.x + x.x - v.x, base.y + x.y - v.y);
+}
+
+// Fixed-tree block sum (deterministic).  All threads must call.
+__device__ inline double block_sum(double v, double* red) {
+  red[threadIdx.x] = v;
+  __syncthreads();
+#pragma unroll
+  for (int s = BLOCK / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+// index i with sl_start[i] <= p < sl_start[i+1]
+__device__ inline int line_of(const int* sl_start, int S, int p) {
+  int lo = 0, hi = S - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (sl_start[mid] <= p) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// f3-gate of one lattice line (reading C10): every band [lo, hi] containing f3 contributes
+// t = 1 strictly inside, 1/2 on an edge (touching bands split 1/2 / 1/2).
+__device__ inline void line_gate(const KParams& p, double f3, int k1, int k2, double* wD, double* wE,
+                                 double* wF) {
+  double d = 0.0, e = 0.0, ff = 0.0;
+  int lo = 0, hi = p.n_ch - 1;       // largest i with lo[i] <= f3
+  if (f3 >= __ldg(p.lo)) {
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (__ldg(p.lo + mid) <= f3) lo = mid; else hi = mid - 1;
+    }
+    for (int c = lo; c >= lo - 1 && c >= 0; --c) {
+      const double l = __ldg(p.lo + c), h = __ldg(p.hi + c);
+      if (f3 >= l && f3 <= h) {
+        const double t = (f3 > l && f3 < h) ? 1.0 : 0.5;
+        d += t * __ldg(p.G + c);
+        if (c == k1) e += t;
+        if (c == k2) ff += t;
+      }
+    }
+  }
+  *wD = d;
+  *wE = e;
+  *wF = ff;
+}
+
+__device__ inline long long gcd_ll(long long a, long long b) {
+  while (b) {
+    long long t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+// ------------------------------------------------------------------------------------------
+// integrand (rows a3-a6)
+
+template <bool COH, int MODE>
+__global__ void __launch_bounds__(BLOCK, 2)
+integrand_kernel(const KParams p, const int* __restrict__ list) {
+  extern __shared__ __align__(16) char smem_raw[];
+  Smem sm;
+  smem_layout(p.tstride, p.tw, p.N, COH, smem_raw, &sm);
+  const int tid = threadIdx.x;
+  const int rid = list[blockIdx.x];
+  const RegionDesc rd = p.desc[rid];
+  const int k1 = rd.k1, k2 = rd.k2, flags = rd.flags;
+  const int N = p.N;
+
+  const double f = __ldg(p.f + rd.kappa);
+  const double lo1 = __ldg(p.lo + k1), lo2 = __ldg(p.lo + k2);
+  const double d1 = __ldg(p.delta + k1), d2 = __ldg(p.delta + k2);
+  // lattice ratio a:b = R1:R2 (coprime); f3 = C + g (a m1 + b m2), exact in fp64 (reading C10)
+  const long long r1 = __ldg(p.rate + k1), r2 = __ldg(p.rate + k2);
+  const long long g0 = gcd_ll(r1, r2);
+  const int a = (int)(r1 / g0), b = (int)(r2 / g0);
+  const double g = d1 / a;                                   // = d2 / b, an integer number of Hz
+  const double C = __dadd_rn(__dadd_rn(__dadd_rn(lo1, lo2), -f), __dadd_rn(0.5 * d1, 0.5 * d2));
+  int inv_a = 0;                                             // a^{-1} mod b
+  if (b > 1) {
+    for (int x = 1; x < b; ++x)
+      if ((long long)a * x % b == 1) { inv_a = x; break; }
+  }
+  const int J = (a + b) * (N - 1) + 1;
+
+  double Dacc = 0.0;
+  double Ghat = 0.0;           // sum_i wD_i |a_i|^2 (G)
+  double2 hsum = make_double2(0.0, 0.0);  // sum_i wE_i a_i (H)
+  long long npts_total = 0;
+  if (COH) {
+    for (int m = tid; m < N; m += BLOCK) {
+      sm.rowacc[m] = make_double2(0.0, 0.0);
+      sm.colacc[m] = make_double2(0.0, 0.0);
+    }
+  }
+
+  for (int seg0 = 0; seg0 < J; seg0 += LINE_CAP) {
+    const int nl = min(LINE_CAP, J - seg0);
+    // ---- line scan: each thread owns two consecutive lines (order-preserving compaction)
+    int cnt[2], first[2];
+    double lwD[2], lwE[2], lwF[2];
+    int2 v = make_int2(0, 0);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int jl = 2 * tid + q;
+      cnt[q] = 0;
+      first[q] = 0;
+      lwD[q] = lwE[q] = lwF[q] = 0.0;
+      if (jl < nl) {
+        const int j = seg0 + jl;
+        // points on the line: a m1 + b m2 = j, 0 <= m1, m2 < N
+        int lowb = j - b * (N - 1);
+        lowb = (lowb <= 0) ? 0 : (lowb + a - 1) / a;
+        const int upb = min(N - 1, j / a);
+        int fm = lowb;
+        if (b > 1) {
+          const int r = (int)(((long long)(j % b) * inv_a) % b);
+          fm = lowb + (((r - lowb) % b) + b) % b;
+        }
+        const int n = (fm <= upb) ? (upb - fm) / b + 1 : 0;
+        if (n > 0) {
+          const double f3 = __dadd_rn(C, g * (double)j);
+          line_gate(p, f3, k1, k2, &lwD[q], &lwE[q], &lwF[q]);
+          if (lwD[q] > 0.0) {
+            cnt[q] = n;
+            first[q] = fm;
+            v.x += 1;
+            v.y += n;
+          }
+        }
+      }
+    }
+    int2 tot;
+    int2 pos = block_scan2(v, sm.scan, &tot);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (cnt[q] > 0) {
+        sm.sl_j[pos.x] = seg0 + 2 * tid + q;
+        sm.sl_first[pos.x] = first[q];
+        sm.sl_start[pos.x] = pos.y;
+        sm.wD[pos.x] = lwD[q];
+        sm.wE[pos.x] = lwE[q];
+        sm.wF[pos.x] = lwF[q];
+        pos.x += 1;
+        pos.y += cnt[q];
+      }
+    }
+    const int S = tot.x, NP = tot.y;
+    if (tid == 0) sm.sl_start[S] = NP;
+    if (COH) {
+      for (int i = tid; i < S; i += BLOCK) sm.lineacc[i] = make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    npts_total += NP;
+    if (NP == 0) continue;
+
+    int tb = 0, tn = 0, tcls = -1;  // resident table: compacted lines [tb, tb + tn), class tcls
+    for (int p0 = 0; p0 < NP;) {
+      // ---- chunk boundaries (block-uniform)
+      const int i_first = line_of(sm.sl_start, S, p0);
+      const int lim = min(i_first + p.tw, S);
+      const int p_end = min(p0 + CP, sm.sl_start[lim]);
+      const int i_last = line_of(sm.sl_start, S, p_end - 1);
+
+      // ---- per-thread points
+      int li[PPT];
+      bool valid[PPT];
+      double uv[PPT], Ssum[PPT], f3v[PPT];
+#pragma unroll
+      for (int q = 0; q < PPT; ++q) {
+        const int idx = p0 + q * BLOCK + tid;
+        valid[q] = idx < p_end;
+        const int i = valid[q] ? line_of(sm.sl_start, S, idx) : i_first;
+        li[q] = i;
+        const int j = sm.sl_j[i];
+        const int m1 = sm.sl_first[i] + b * (valid[q] ? idx - sm.sl_start[i] : 0);
+        const int m2 = (j - a * m1) / b;
+        const double f1 = __dadd_rn(lo1, __dmul_rn((double)m1 + 0.5, d1));   // C6 bin centres
+        const double f2 = __dadd_rn(lo2, __dmul_rn((double)m2 + 0.5, d2));
+        const double u = __dadd_rn(f1, -f), w = __dadd_rn(f2, -f);
+        uv[q] = __dmul_rn(u, w);
+        Ssum[q] = __dadd_rn(f1, f2);
+        f3v[q] = __dadd_rn(C, g * (double)j);
+      }
+
+      double yr[PPT], yi[PPT], th[PPT];
+#pragma unroll
+      for (int q = 0; q < PPT; ++q) {
+        yr[q] = (MODE == MODE_UNIT) ? 1.0 : 0.0;
+        yi[q] = 0.0;
+        th[q] = 0.0;
+      }
+
+      if (MODE != MODE_UNIT) {
+        for (int s = 0; s < p.n_span; ++s) {
+          const int cls = __ldg(p.cls + s);
+          if (MODE == MODE_SEGMENT &&
+              (cls != tcls || i_first < tb || i_last >= tb + tn)) {
+            // ---- (re)build the envelope table rows for compacted lines [tb, tb + tn)
+            __syncthreads();
+            tb = i_first;
+            tn = (p.n_cls == 1) ? min(p.tw, S - i_first) : (i_last - i_first + 1);
+            tcls = cls;
+            const int Kc = __ldg(p.Kc + cls);
+            const int Kp = (Kc + 1) & ~1;
+            const double* lnA = p.lnA + (size_t)cls * p.kstride;
+            const double* zt = p.zeta + (size_t)cls * p.kstride;
+            for (int e = tid; e < tn * Kp; e += BLOCK) {
+              const int row = e / Kp, ii = e - row * Kp;
+              const int k = Kp - 1 - ii;
+              const double f3 = __dadd_rn(C, g * (double)sm.sl_j[tb + row]);
+              sm.T[row * p.tstride + ii] =
+                  (k < Kc) ? exp(__ldg(lnA + k) - __ldg(zt + k) * f3) : 0.0;
+            }
+            __syncthreads();
+          }
+          const double A2 = __ldg(p.A2 + s), A3 = __ldg(p.A3 + s);
+          const double Eh = __ldg(p.Eh + s), ah = __ldg(p.ah + s), gh = __ldg(p.gh + s);
+          const int Ks = __ldg(p.K + s);
+          double x[PPT], sn[PPT], cs[PPT];
+#pragma unroll
+          for (int q = 0; q < PPT; ++q) {
+            x[q] = uv[q] * fma(A3, Ssum[q], A2);     // chi h / pi  (Eq. 5 times h / pi)
+            sincospi(x[q], &sn[q], &cs[q]);          // z = e^{i chi h}
+          }
+          double accr[PPT], acci[PPT];
+          if (MODE == MODE_SEGMENT) {
+            // ---- Goertzel over the K_s segments (Eqs. 8-9 with I_k = I_0 w^k)
+            const int Kp = (__ldg(p.Kc + cls) + 1) & ~1;
+            double c2[PPT], b1[PPT], b2[PPT];
+            const double2* rowp[PPT];
+#pragma unroll
+            for (int q = 0; q < PPT; ++q) {
+              c2[q] = cs[q] + cs[q];
+              b1[q] = 0.0;
+              b2[q] = 0.0;
+              rowp[q] = (const double2*)(sm.T + (li[q] - tb) * p.tstride);
+            }
+            const int npair = Kp >> 1;
+            for (int i2 = 0; i2 < npair - 1; ++i2) {
+#pragma unroll
+              for (int q = 0; q < PPT; ++q) {
+                const double2 t = rowp[q][i2];
+                const double n0 = fma(c2[q], b1[q], t.x - b2[q]);
+                const double n1 = fma(c2[q], n0, t.y - b1[q]);
+                b2[q] = n0;
+                b1[q] = n1;
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < PPT; ++q) {
+              const double2 t = rowp[q][npair - 1];
+              const double n0 = fma(c2[q], b1[q], t.x - b2[q]);   // b_1
+              // sum_k a'_k z^k = a'_0 + z b_1 - b_2
+              accr[q] = fma(cs[q], n0, t.y - b1[q]);
+              acci[q] = sn[q] * n0;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < PPT; ++q) {
+            const double px = CUDART_PI * x[q];     // chi h
+            double mr, mi;
+            if (MODE == MODE_SEGMENT) {
+              // I_0 = (w - 1)/(i chi - alpha) = h (w - 1) conj(d) / |d|^2, d = -alpha h + i chi h
+              const double wr1 = fma(Eh, cs[q], -1.0), wi = Eh * sn[q];
+              const double inv = gh / fma(px, px, ah * ah);     // gamma_s h / |d|^2
+              const double nr = fma(wi, px, -ah * wr1);
+              const double ni = -fma(px, wr1, ah * wi);
+              mr = (nr * accr[q] - ni * acci[q]) * inv;
+              mi = (nr * acci[q] + ni * accr[q]) * inv;
+            } else {
+              // Maclaurin (Eq. 4): mu = eta - (P C f3 / alpha)(eta - eta2), eta = (e^{(i chi - a)L}-1)/(i chi - a)
+              const double aL = __ldg(p.aL + s);
+              const double xl = x[q] * Ks;        // chi L / pi
+              double sl, cl;
+              sincospi(xl, &sl, &cl);
+              const double e1 = exp(-aL), e2 = e1 * e1;
+              // eta / h = (e1 cis(chi L) - 1) / ((i chi - alpha) h): multiply by conj(d) / |d|^2
+              const double ar = -ah, ai = px;     // d = (i chi - alpha) h
+              const double den1 = 1.0 / fma(ai, ai, ar * ar);
+              const double n1r = fma(e1, cl, -1.0), n1i = e1 * sl;
+              const double eta_r = (n1r * ar + n1i * ai) * den1;
+              const double eta_i = (n1i * ar - n1r * ai) * den1;
+              const double br = -2.0 * ah;
+              const double den2 = 1.0 / fma(ai, ai, br * br);
+              const double n2r = fma(e2, cl, -1.0), n2i = e2 * sl;
+              const double et2_r = (n2r * br + n2i * ai) * den2;
+              const double et2_i = (n2i * br - n2r * ai) * den2;
+              const double cf = __ldg(p.mac_c + s) * f3v[q];
+              // (values above are eta / h; gh = gamma h restores the scale)
+              mr = (eta_r - cf * (eta_r - et2_r)) * gh;
+              mi = (eta_i - cf * (eta_i - et2_i)) * gh;
+            }
+            // Y += gamma_s mu_s e^{i theta_s}, theta_s = pi * th (reading C3)
+            double ps, pc;
+            sincospi(th[q], &ps, &pc);
+            yr[q] = fma(mr, pc, fma(-mi, ps, yr[q]));
+            yi[q] = fma(mr, ps, fma(mi, pc, yi[q]));
+            double t2 = fma(x[q], (double)Ks, th[q]);   // theta_{s+1} = theta_s + chi_s L_s
+            th[q] = t2 - 2.0 * rint(0.5 * t2);          // exact reduction mod 2 (units of pi)
+          }
+        }
+      }
+
+      // ---- D accumulation
+#pragma unroll
+      for (int q = 0; q < PPT; ++q) {
+        if (valid[q]) Dacc = fma(sm.wD[li[q]], fma(yr[q], yr[q], yi[q] * yi[q]), Dacc);
+      }
+
+      if (COH) {
+#pragma unroll
+        for (int q = 0; q < PPT; ++q)
+          sm.ybuf[q * BLOCK + tid] = valid[q] ? make_double2(yr[q], yi[q]) : make_double2(0.0, 0.0);
+        __syncthreads();
+        // lines (G, H): one thread per line in the chunk, points in order
+        if (flags & (NEED_G | NEED_H)) {
+          for (int i = i_first + tid; i <= i_last; i += BLOCK) {
+            const int s0 = max(sm.sl_start[i], p0), s1 = min(sm.sl_start[i + 1], p_end);
+            double2 acc = sm.lineacc[i];
+            for (int t = s0; t < s1; ++t) {
+              const double2 y = sm.ybuf[t - p0];
+              acc.x += y.x;
+              acc.y += y.y;
+            }
+            sm.lineacc[i] = acc;
+          }
+        }
+        // rows (E): r[m2] += sum over the chunk's lines of wE Y(m1, m2), line order
+        if (flags & NEED_E) {
+          for (int m2 = tid; m2 < N; m2 += BLOCK) {
+            double2 acc = sm.rowacc[m2];
+            for (int i = i_first; i <= i_last; ++i) {
+              const double w = sm.wE[i];
+              if (w == 0.0) continue;
+              const int num = sm.sl_j[i] - b * m2;
+              if (num < 0 || num % a) continue;
+              const int m1 = num / a;
+              if (m1 >= N) continue;
+              const int idx = sm.sl_start[i] + (m1 - sm.sl_first[i]) / b;
+              if (m1 < sm.sl_first[i] || idx < p0 || idx >= p_end) continue;
+              const double2 y = sm.ybuf[idx - p0];
+              acc.x = fma(w, y.x, acc.x);
+              acc.y = fma(w, y.y, acc.y);
+            }
+            sm.rowacc[m2] = acc;
+          }
+        }
+        // columns (F): c[m1] += sum over the chunk's lines of wF Y(m1, m2)
+        if (flags & NEED_F) {
+          for (int m1 = tid; m1 < N; m1 += BLOCK) {
+            double2 acc = sm.colacc[m1];
+            for (int i = i_first; i <= i_last; ++i) {
+              const double w = sm.wF[i];
+              if (w == 0.0) continue;
+              const int num = sm.sl_j[i] - a * m1;
+              if (num < 0 || num % b) continue;
+              const int m2 = num / b;
+              if (m2 >= N || m1 < sm.sl_first[i]) continue;
+              const int idx = sm.sl_start[i] + (m1 - sm.sl_first[i]) / b;
+              if (idx < p0 || idx >= p_end) continue;
+              const double2 y = sm.ybuf[idx - p0];
+              acc.x = fma(w, y.x, acc.x);
+              acc.y = fma(w, y.y, acc.y);
+            }
+            sm.colacc[m1] = acc;
+          }
+        }
+        __syncthreads();
+      }
+      p0 = p_end;
+    }
+    if (COH && (flags & (NEED_G | NEED_H)) && tid == 0) {
+      for (int i = 0; i < S; ++i) {
+        const double2 av = sm.lineacc[i];
+        Ghat = fma(sm.wD[i], fma(av.x, av.x, av.y * av.y), Ghat);
+        hsum.x = fma(sm.wE[i], av.x, hsum.x);
+        hsum.y = fma(sm.wE[i], av.y, hsum.y);
+      }
+    }
+    __syncthreads();
+  }
+
+  const double Dsum = block_sum(Dacc, sm.red);
+  if (tid == 0) {
+    double* out = p.partials + (size_t)rid * 6;
+    double E = 0.0, F = 0.0;
+    if (COH) {
+      if (flags & NEED_E)
+        for (int m = 0; m < N; ++m) E = fma(sm.rowacc[m].x, sm.rowacc[m].x, fma(sm.rowacc[m].y, sm.rowacc[m].y, E));
+      if (flags & NEED_F)
+        for (int m = 0; m < N; ++m) F = fma(sm.colacc[m].x, sm.colacc[m].x, fma(sm.colacc[m].y, sm.colacc[m].y, F));
+    }
+    out[0] = Dsum * d1 * d2;                                         // D_w
+    out[1] = (COH && (flags & NEED_E)) ? E * d1 * d1 * d2 : 0.0;     // E_w
+    out[2] = (COH && (flags & NEED_F)) ? F * d2 * d2 * d1 : 0.0;     // F_w
+    out[3] = (COH && (flags & NEED_G)) ? Ghat * d1 * d1 * d1 : 0.0;  // G_w (k1 == k2)
+    out[4] = (COH && (flags & NEED_H)) ? (hsum.x * hsum.x + hsum.y * hsum.y) * (d1 * d2) * (d1 * d2) : 0.0;
+    out[5] = (double)npts_total;
+  }
+}
+
+template <bool COH, int MODE>
+static int launch_one(const KParams& p, const int* list, long long n_list, cudaStream_t st) {
+  const size_t smem = integrand_smem_bytes(p.tstride, p.tw, p.N, COH);
+  auto kern = integrand_kernel<COH, MODE>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return -1;
+  const long long max_grid = 0x7fffffffLL;
+  for (long long off = 0; off < n_list; off += max_grid) {
+    const unsigned grid = (unsigned)std::min(max_grid, n_list - off);
+    kern<<<grid, BLOCK, smem, st>>>(p, list + off);
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_integrand(const KParams& p, const int* list, long long n_list, bool coherent, void* stream,
+                     int* n_launches) {
+  if (n_list <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  *n_launches += 1;
+  if (coherent) {
+    if (p.mode == MODE_SEGMENT) return launch_one<true, MODE_SEGMENT>(p, list, n_list, st);
+    if (p.mode == MODE_MACLAURIN) return launch_one<true, MODE_MACLAURIN>(p, list, n_list, st);
+    return launch_one<true, MODE_UNIT>(p, list, n_list, st);
+  }
+  if (p.mode == MODE_SEGMENT) return launch_one<false, MODE_SEGMENT>(p, list, n_list, st);
+  if (p.mode == MODE_MACLAURIN) return launch_one<false, MODE_MACLAURIN>(p, list, n_list, st);
+  return launch_one<false, MODE_UNIT>(p, list, n_list, st);
+}
+
+// ------------------------------------------------------------------------------------------
+// per-COI assembly (row a7)
+
+__global__ void __launch_bounds__(BLOCK) reduce_kernel(const RParams p) {
+  __shared__ double red[6][BLOCK];
+  const int ci = blockIdx.x;
+  const long long r0 = p.coi_off[ci], r1 = p.coi_off[ci + 1];
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  for (long long r = r0 + threadIdx.x; r < r1; r += BLOCK) {
+    const RegionDesc rd = p.desc[r];
+    const double* q = p.partials + (size_t)r * 6;
+    const double G1 = p.G[rd.k1], G2 = p.G[rd.k2], R1 = p.R[rd.k1], R2 = p.R[rd.k2];
+    const double ph1 = p.phi[rd.k1], ph2 = p.phi[rd.k2], ps1 = p.psi[rd.k1];
+    // Eq. 15 with reading C2 (PSD normalisation, one 1/R_i per cumulant-tied channel)
+    acc[0] += 16.0 / 27.0 * G1 * G2 * q[0];
+    acc[1] += 16.0 / 27.0 * ph1 * G1 * G1 * G2 * q[1] / R1;
+    acc[2] += 32.0 / 81.0 * ph2 * G2 * G2 * G1 * q[2] / R2;
+    acc[3] += 16.0 / 81.0 * ph1 * G1 * G1 * q[3] / R1;
+    acc[4] += 16.0 / 81.0 * ps1 * G1 * G1 * G1 * q[4] / (R1 * R1);
+    acc[5] += q[5];
+  }
+#pragma unroll
+  for (int k = 0; k < 6; ++k) red[k][threadIdx.x] = acc[k];
+  __syncthreads();
+  for (int s = BLOCK / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const int kappa = p.coi[ci];
+    const double Pk = p.P[kappa];
+    const double scale = p.R[kappa] / (Pk * Pk * Pk);   // P_NLI = R G_NLI (C1); Eq. 11
+    double e = 0.0;
+    for (int k = 0; k < 5; ++k) {
+      const double t = red[k][0] * scale;
+      if (p.terms) p.terms[(size_t)ci * 5 + k] = t;
+      e += t;
+    }
+    p.eta[ci] = e;
+    p.npts[ci] = red[5][0];
+  }
+}
+
+int launch_reduce(const RParams& p, void* stream) {
+  if (p.n_coi <= 0) return 0;
+  reduce_kernel<<<p.n_coi, BLOCK, 0, (cudaStream_t)stream>>>(p);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace isrs

@@ -1,0 +1,103 @@
+"""C-ABI library checks that need no GPU: it loads, exports every symbol include/isrs_egn.h
+declares, and rejects invalid input with the documented status before touching CUDA."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "isrs_egn.h")
+
+
+@pytest.fixture(scope="module")
+def abi():
+    from paper_2412_11614_b200 import build
+    build.build()
+    from paper_2412_11614_b200 import _abi
+    return _abi
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"ISRS_EGN_API\s+[\w\s\*]*?\b(isrs_egn_\w+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for s in ("isrs_egn_create", "isrs_egn_nli", "isrs_egn_destroy"):
+        assert s in syms
+    assert len(syms) == 9
+
+
+def test_library_exports_every_declared_symbol(abi):
+    lib = ctypes.CDLL(abi.LIB_PATH)
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+    assert sorted(abi.EXPORTED) == declared_symbols()
+
+
+def test_library_is_sm100a_only(abi):
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", abi.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert "sm_90" not in out and "sm_80" not in out
+
+
+def test_strerror(abi):
+    assert abi.lib.isrs_egn_strerror(0) == b"ok"
+    assert abi.lib.isrs_egn_strerror(-2) == b"channel bands overlap"
+
+
+def _create(abi, link, **kw):
+    pa = abi.ProblemArrays(link)
+    n = abi.numerics(kw.get("grid_n", link.grid_n), kw.get("dz", 1000.0), kw.get("precision", 64),
+                     kw.get("mu_mode", 0))
+    h = ctypes.c_void_p()
+    rc = abi.lib.isrs_egn_create(ctypes.byref(pa.struct), ctypes.byref(n), 0, ctypes.byref(h))
+    return rc, abi.lib.isrs_egn_last_error().decode(), h
+
+
+def test_validation_errors_before_any_cuda(abi):
+    from workloads import tiny_link
+    l = tiny_link(n_ch=3, n_span=2, grid_n=8)
+    rc, msg, h = _create(abi, l, grid_n=7)
+    assert rc == abi.EINVAL and "even" in msg and not h.value
+    rc, msg, _ = _create(abi, l, dz=0.0)
+    assert rc == abi.EINVAL and "delta_z" in msg
+    rc, msg, _ = _create(abi, l, precision=16)
+    assert rc == abi.EUNSUPPORTED
+    bad = l.with_(f_center_hz=l.f_center_hz + 0.25)
+    rc, msg, _ = _create(abi, bad)
+    assert rc == abi.EINVAL and "integer" in msg
+    over = l.with_(symbol_rate_hz=np.full(3, 128e9))
+    rc, msg, _ = _create(abi, over, grid_n=8)
+    assert rc == abi.EOVERLAP and "overlap" in msg
+    neg = l.with_(alpha_per_m=np.array([4.6e-5, 0.0]))
+    rc, msg, _ = _create(abi, neg)
+    assert rc == abi.EINVAL and "alpha_per_m[1]" in msg
+    unsorted = l.with_(f_center_hz=l.f_center_hz[::-1].copy())
+    rc, msg, _ = _create(abi, unsorted)
+    assert rc == abi.EINVAL and "increasing" in msg
+    lat = l.with_(symbol_rate_hz=np.full(3, 64e9 + 2))
+    rc, msg, _ = _create(abi, lat)
+    assert rc == abi.EINVAL and "2 grid_n" in msg
+
+
+def test_destroy_null_safe(abi):
+    abi.lib.isrs_egn_destroy(None)
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2412_11614_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".h", ".cpp")):
+                txt = open(os.path.join(dp, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+(oracle|workloads)\b", txt, re.M), f
+    for dp, _, fs in os.walk(os.path.join(ROOT, "oracle")):
+        for f in fs:
+            if f.endswith(".py"):
+                txt = open(os.path.join(dp, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+paper_2412_11614_b200\b", txt, re.M), f

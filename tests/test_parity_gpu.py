@@ -1,0 +1,175 @@
+"""Parity of the CUDA path (through the C ABI) against the oracle, on the same seeded inputs.
+
+Bar (BASELINE.json north_star): |eta_gpu - eta_oracle| / eta <= 1e-10 for every COI.
+At full BASELINE sizes the oracle cannot finish whole configs, so the per-region partial
+integrals written by the very nli() launch bench.py times are sampled and recomputed one by
+one by the oracle.  Their tolerance is max(1e-10, 64 eps Theta_max): Theta_max is the largest
+accumulated dispersion phase sum_s |chi_s| L_s in the region; a 1-ulp change of any input moves
+Y there by ~eps Theta_max (SURVEY [X5b]), so no fp64 evaluation of Eqs. 8-22 is more
+determined than that.  Whole-eta parity stays at 1e-10 on every config the
+oracle finishes in seconds.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import egn, fwm  # noqa: E402
+from workloads import bj_config, tiny_link  # noqa: E402
+
+EPS = np.finfo(np.float64).eps
+TOL_ETA = 1e-10
+
+
+@pytest.fixture(scope="module")
+def isrs():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2412_11614_b200 import build
+    build.build()
+    import paper_2412_11614_b200 as m
+    return m
+
+
+def gpu_eta(isrs, link, coi=None, **kw):
+    with isrs.Engine(link, **kw) as e:
+        eta, terms = e.nli(coi=coi, terms=True)
+        torch.cuda.synchronize()
+        return eta.cpu().numpy(), terms.cpu().numpy()
+
+
+TINY = {
+    "uniform_64gbd_2span": dict(n_ch=3, rates_gbd=(64,), n_span=2, grid_n=8, fmts=("16qam",)),
+    "three_islands_96gbd": dict(n_ch=4, rates_gbd=(96,), n_span=3, grid_n=8, fmts=("qpsk", "64qam")),
+    "mixed_rates_guard": dict(n_ch=5, rates_gbd=(32, 64, 96), guard_ghz=12.5, n_span=2, grid_n=8,
+                              fmts=("qpsk", "16qam", "64qam")),
+    "touching_bands": dict(n_ch=4, rates_gbd=(32,), guard_ghz=0.0, n_span=2, grid_n=8,
+                           fmts=("qpsk",)),
+    "random_spans_multiclass": dict(n_ch=3, rates_gbd=(64, 32), guard_ghz=20.0, n_span=4, grid_n=8,
+                                    random_spans=True, fmts=("16qam", "gauss")),
+    "ragged_chunks_N34": dict(n_ch=2, rates_gbd=(68,), spacing_ghz=100.0, n_span=2, grid_n=34,
+                              fmts=("64qam",), tilt_db=2.0),
+    "single_channel_N64": dict(n_ch=1, rates_gbd=(64,), n_span=3, grid_n=64, fmts=("qpsk",)),
+    "strong_isrs": dict(n_ch=3, rates_gbd=(96,), spacing_ghz=100.0, n_span=2, grid_n=8,
+                        cr_w_km_thz=5.0, power_dbm=12.0, fmts=("16qam",)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(TINY))
+def test_eta_parity_tiny(isrs, name):
+    link = tiny_link(**TINY[name])
+    e_o, t_o = egn.eta(link)
+    e_g, t_g = gpu_eta(isrs, link)
+    rel = np.abs(e_g - e_o) / e_o
+    assert np.all(rel <= TOL_ETA), (name, rel)
+    scale = np.abs(t_o).sum(axis=1, keepdims=True)
+    assert np.all(np.abs(t_g - t_o) <= TOL_ETA * scale), (name, t_g, t_o)
+
+
+def test_eta_parity_c1_full(isrs):
+    link = bj_config("c1")
+    e_o, t_o = egn.eta(link)
+    e_g, t_g = gpu_eta(isrs, link)
+    assert np.all(np.abs(e_g - e_o) / e_o <= TOL_ETA), (e_g, e_o)
+
+
+def test_eta_parity_coi_subset_and_order(isrs):
+    link = tiny_link(**TINY["mixed_rates_guard"])
+    coi = [4, 0, 2]
+    e_o, _ = egn.eta(link, coi=coi)
+    e_g, _ = gpu_eta(isrs, link, coi=coi)
+    assert np.all(np.abs(e_g - e_o) / e_o <= TOL_ETA)
+
+
+def test_unit_link_hook_matches_closed_form(isrs):
+    # pin P6 through the CUDA path: Y := 1, single channel
+    for fmt, (phi, psi) in (("qpsk", (-1.0, 4.0)), ("16qam", (-0.68, 2.08))):
+        link = tiny_link(n_ch=1, rates_gbd=(48,), n_span=1, grid_n=64, fmts=(fmt,))
+        e_g, t_g = gpu_eta(isrs, link, flags=isrs.FLAG_UNIT_LINK)
+        e_o, _ = egn.eta(link, mu_mode="unit")
+        assert abs(e_g[0] - e_o[0]) <= 1e-13
+        assert abs(e_g[0] - egn.unit_link_eta(phi, psi)) < 2e-5
+
+
+def test_maclaurin_mode_parity(isrs):
+    link = tiny_link(**TINY["three_islands_96gbd"])
+    e_o, _ = egn.eta(link, mu_mode="maclaurin")
+    e_g, _ = gpu_eta(isrs, link, mu_mode=isrs.MU_MACLAURIN)
+    assert np.all(np.abs(e_g - e_o) / e_o <= TOL_ETA)
+
+
+def test_gn_reduction_bitwise_and_determinism(isrs):
+    link = tiny_link(n_ch=3, rates_gbd=(64,), n_span=2, grid_n=16, fmts=("gauss",))
+    e1, t1 = gpu_eta(isrs, link)
+    e2, t2 = gpu_eta(isrs, link)
+    assert np.array_equal(e1, e2) and np.array_equal(t1, t2)
+    assert np.array_equal(e1, t1[:, 0]) and np.all(t1[:, 1:] == 0.0)
+    lq = link.with_(phi=np.full(3, -0.68), psi=np.full(3, 2.08))
+    _, tq = gpu_eta(isrs, lq)
+    assert np.array_equal(tq[:, 0], t1[:, 0])
+
+
+def test_errors_surface_from_nli(isrs):
+    link = tiny_link(n_ch=3, n_span=1, grid_n=8)
+    with isrs.Engine(link) as e:
+        with pytest.raises(isrs.IsrsEgnError):
+            e.nli(coi=[3])
+
+
+# ------------------------------------------------------------------ full BASELINE sizes
+
+def theta_max(link, kappa, k1, k2):
+    c = egn.canonicalize(link)
+    F1, F2, _ = egn.region_points(c, kappa, k1, k2)
+    th = 0.0
+    for sp in c.spans:
+        th = th + np.abs(fwm.chi(F1, F2, c.f[kappa], sp["beta2"], sp["beta3"])) * sp["L"]
+    return float(np.max(th))
+
+
+def sampled_regions(n, kappas):
+    out = []
+    for k in kappas:
+        out += [(k, k, k), (k, min(k + 1, n - 1), k), (k, k, max(k - 1, 0)),
+                (k, min(k + 3, n - 1), max(k - 2, 0)), (k, max(k - 5, 0), max(k - 5, 0))]
+    return out
+
+
+FULL = {
+    "c2": (None, (0, 19)),
+    "c3": (None, (50,)),
+    "c4": (None, (7, 41)),
+    "c5": ([0, 100, 199], (100, 199)),
+}
+
+
+@pytest.mark.parametrize("cfg", sorted(FULL))
+def test_full_size_region_parity(isrs, cfg):
+    link = bj_config(cfg)
+    coi, kappas = FULL[cfg]
+    with isrs.Engine(link) as e:
+        eta = e.nli(coi=coi)
+        torch.cuda.synchronize()
+        eta = eta.cpu().numpy()
+        assert np.all(np.isfinite(eta)) and np.all(eta > 0)
+        regs = sampled_regions(link.n_ch, kappas)
+        got = e.region_partials(regs)
+        pts, pspans, nreg = e.work()
+    assert pspans == pts * link.n_span and nreg > 0
+    for (kappa, k1, k2), g in zip(regs, got):
+        want, npts = egn.region_partials(link, kappa, k1, k2)
+        assert g[5] == npts, (cfg, kappa, k1, k2)
+        tol = max(TOL_ETA, 64 * EPS * theta_max(link, kappa, k1, k2))
+        scale = max(np.max(np.abs(want)), 1e-300)
+        for t in range(5):
+            assert abs(g[t] - want[t]) <= tol * max(abs(want[t]), 1e-300) or \
+                abs(g[t] - want[t]) <= 1e-13 * scale, (cfg, (kappa, k1, k2), t, g[t], want[t], tol)
+
+
+def test_full_size_determinism_c2(isrs):
+    link = bj_config("c2")
+    with isrs.Engine(link) as e:
+        a = e.nli().cpu().numpy()
+        b = e.nli().cpu().numpy()
+    assert np.array_equal(a, b)
