@@ -1,0 +1,293 @@
+#!/usr/bin/env python
+"""Benchmark of the ISRS EGN hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+One step = one pass of the whole hot path (rows a2-a7: the nli() call: integrand kernels over
+every region of every COI + per-COI assembly) over BASELINE.json configs[1] (c2: C-band 40 x
+64 GBd, 10 x 80 km, N = 128, all 40 channels as COI), inputs resident in HBM.  The path
+partitions into independent links / COI sets; at N GPUs every rank evaluates its own copy of
+the link (weak scaling, no collective on the data path).
+
+Prints ONE JSON line (rank 0).  value = integrand point-spans/s over all ranks; the other parts
+of the BASELINE metric (channels/s, % of FP64 peak) are extra keys and in `roofline`.
+`--impl reference` times the oracle (oracle/, numpy fp64, the plain CPU reference) on a bounded
+sample of the same workload on this host's cores.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "integrand point-spans/sec and NLI-eta channels/sec (fp64), % of FP64 peak"
+UNIT = "point-spans/s"
+# FP64 peak derived from unit counts and clocks (B200_PROFILING.md: 148 SMs, 1965 MHz max SM
+# clock; 64 FP64 FMA lanes per SM): 148 * 64 * 2 * 1.965e9 = 37.2 TFLOP/s.
+SMS, FP64_LANES, SM_MAX_MHZ = 148, 64, 1965.0
+
+
+def fp64_peak_tflops(mhz=SM_MAX_MHZ):
+    return SMS * FP64_LANES * 2 * mhz * 1e6 / 1e12
+
+
+def algorithmic_flops_per_point(link):
+    """Per grid point summed over spans: 3 flops per segment of the second-order recurrence
+    (one DFMA + one DADD, Goertzel form of Eqs. 8-9) plus 40 flops of per-span arithmetic (chi,
+    I_0, mu, Y accumulation, phase); the two sincospi per span are not counted."""
+    K = np.ceil(np.asarray(link.length_m) / link.delta_z_m)
+    Kp = 2 * np.ceil(K / 2)
+    return float(np.sum(3 * (Kp - 1) + 40))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = []
+        reasons = set()
+        smax = None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                smax = float(r[1])
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        dist.init_process_group(backend)
+    return ws, rank, local
+
+
+def oracle_sample(link, seconds_target, regions=None):
+    """Time the oracle (closed mode, literal Eqs. 8-10) on a bounded sample of regions of the
+    workload.  Returns (point-spans/s, point-spans, seconds, sample description)."""
+    from oracle import egn
+    c = egn.canonicalize(link)
+    mid = link.n_ch // 2
+    cand = regions or [(mid, mid, mid), (mid, mid + 1, mid - 1), (mid, mid - 3, mid + 2),
+                       (mid, 0, link.n_ch - 1), (mid, mid + 5, mid + 5), (mid, 2, mid)]
+    done, pspans, t0 = [], 0, time.perf_counter()
+    for reg in cand:
+        _, npts = egn.region_partials(link, *reg)
+        pspans += npts * link.n_span
+        done.append(reg)
+        if time.perf_counter() - t0 > seconds_target:
+            break
+    dt = time.perf_counter() - t0
+    del c
+    return pspans / dt, pspans, dt, f"oracle closed mode on regions (kappa,k1,k2)={done} of {link.name}"
+
+
+def run_reference(args, link, ws, rank):
+    if rank != 0:
+        return
+    steps, warm = args.steps, args.warmup
+    per_step = []
+    pspans_tot = 0
+    for i in range(warm + steps):
+        rate, ps, dt, desc = oracle_sample(link, args.ref_seconds, regions=[(link.n_ch // 2,) * 3])
+        if i >= warm:
+            per_step.append(dt)
+            pspans_tot += ps
+    value = pspans_tot / sum(per_step)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+            "steps": steps, "warmup": warm, "ms_per_step": 1e3 * float(np.mean(per_step)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_desc(link, args),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": desc + " per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_desc(link, args):
+    return {"workload": f"{link.name}: {link.n_ch} ch x {int(link.symbol_rate_hz[0] / 1e9)} GBd, "
+                        f"{link.n_span} spans, N={link.grid_n}, dz={link.delta_z_m:g} m, all channels as COI",
+            "n_ch": link.n_ch, "n_span": link.n_span, "grid_n": link.grid_n,
+            "n_coi": link.n_ch, "seed": link.seed,
+            "l2": "flushed between timed steps (256 MiB write, outside the step events)",
+            "parallelism": f"replicas x{args.gpus} (independent links, weak scaling)"}
+
+
+def run_ours(args, link, ws, rank, local):
+    import torch
+    import paper_2412_11614_b200 as isrs
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    eng = isrs.Engine(link, device=local)
+    n = link.n_ch
+    eta = torch.empty(n, dtype=torch.float64, device=dev)
+    terms = torch.empty((n, 5), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        eng.nli_into(eta.data_ptr(), terms.data_ptr(), None, stream.cuda_stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            flush.zero_()
+            step()
+    torch.cuda.synchronize()
+    pts, pspans, nreg = eng.work()
+    launches_per_step = eng.last_launch_count()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    kern_ms = []
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    with torch.cuda.stream(stream):
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+            kms, kps = eng.last_kernel_ms()          # events inside the library, same stream
+            kern_ms.append((kms, kps))
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if ws > 1:
+        torch.distributed.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = float(np.mean(step_ms))
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(t.item())
+    eta_host = eta.cpu().numpy()
+
+    # roofline of the dominant kernel (integrand over D-only regions)
+    kd_ms = float(np.mean([k[0][0] for k in kern_ms]))
+    kc_ms = float(np.mean([k[0][1] for k in kern_ms]))
+    kr_ms = float(np.mean([k[0][2] for k in kern_ms]))
+    ps_d = kern_ms[-1][1][0]
+    fpp = algorithmic_flops_per_point(link) / link.n_span      # flops per point-span (mean)
+    ach = ps_d * fpp / (kd_ms * 1e-3) / 1e12
+    peak = fp64_peak_tflops()
+
+    # end to end through the public API with host buffers: create + nli + D2H + destroy
+    e2e = None
+    if not args.no_e2e:
+        pa = isrs.ProblemArrays(link)
+        h2d = pa.nbytes()
+        t_e2e = []
+        for k in range(max(1, min(3, args.steps))):
+            t0 = time.perf_counter()
+            isrs.eta_host(link, device=local)
+            t_e2e.append(time.perf_counter() - t0)
+        e2e = {"value": ws * pspans / float(np.median(t_e2e)), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": 8 * n,
+               "note": "isrs_egn_eta_host(): validate + region plan + H2D + precompute + nli + D2H + free"}
+
+    if rank == 0:
+        value = ws * pspans / (ms_max * 1e-3)
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config_desc(link, args),
+                "channels_per_s": ws * n / (ms_max * 1e-3),
+                "point_spans_per_step": pspans, "points_per_step": pts, "regions_per_step": nreg,
+                "kernel_ms": {"integrand_D": kd_ms, "integrand_coherent": kc_ms, "reduce": kr_ms},
+                "roofline": {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                             "frac": ach / peak, "traffic": None,
+                             "kernel": "isrs::integrand_kernel<false,0> (D-only regions)",
+                             "flops_per_point_span": fpp,
+                             "peak_note": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz"},
+                "pct_fp64_peak": 100.0 * ach / peak,
+                "gpu_launches": launches_per_step * args.steps,
+                "clocks": clk, "e2e": e2e,
+                "eta_db_first_mid_last": [float(10 * np.log10(eta_host[i])) for i in (0, n // 2, n - 1)]}
+        if not args.no_cpu:
+            rate, ps, dt, desc = oracle_sample(link, args.ref_seconds)
+            line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                    "sample": f"{desc}; {ps} point-spans in {dt:.1f} s"}
+        print(json.dumps(line), flush=True)
+    eng.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    from workloads import bj_config
+    link = bj_config(args.config)
+    ws, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, link, ws, rank)
+    else:
+        run_ours(args, link, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -24,6 +24,11 @@ def library_path():
     return _abi.LIB_PATH
 
 
+def load():
+    """Load libisrs_egn.so now (raises ImportError when it is missing: no CPU fallback)."""
+    return _abi.get()
+
+
 class Engine:
     """Handle over one link (isrs_egn_create / isrs_egn_nli / isrs_egn_destroy)."""
 
@@ -37,7 +42,7 @@ class Engine:
         self.n_span = self._pa.struct.n_span
         self.device = device
         h = ctypes.c_void_p()
-        _abi.check(_abi.lib.isrs_egn_create(ctypes.byref(self._pa.struct), ctypes.byref(n), device,
+        _abi.check(_abi.get().isrs_egn_create(ctypes.byref(self._pa.struct), ctypes.byref(n), device,
                                             ctypes.byref(h)))
         self._h = h
 
@@ -49,7 +54,7 @@ class Engine:
             c = np.ascontiguousarray(np.asarray(coi, dtype=np.int32))
             n, cp = len(c), c.ctypes.data_as(_abi._ip)
             self._coi_keep = c
-        _abi.check(_abi.lib.isrs_egn_nli(self._h, n, cp, ctypes.c_void_p(eta_ptr),
+        _abi.check(_abi.get().isrs_egn_nli(self._h, n, cp, ctypes.c_void_p(eta_ptr),
                                          ctypes.c_void_p(terms_ptr or None),
                                          ctypes.c_void_p(stream or None)))
 
@@ -69,7 +74,7 @@ class Engine:
         r = np.asarray(regions, dtype=np.int32).reshape(-1, 3)
         k, a, b = (np.ascontiguousarray(r[:, i]) for i in range(3))
         out = np.zeros((len(r), 6))
-        _abi.check(_abi.lib.isrs_egn_region_partials(
+        _abi.check(_abi.get().isrs_egn_region_partials(
             self._h, len(r), k.ctypes.data_as(_abi._ip), a.ctypes.data_as(_abi._ip),
             b.ctypes.data_as(_abi._ip), out.ctypes.data_as(_abi._dp)))
         return out
@@ -77,15 +82,22 @@ class Engine:
     def work(self):
         """(points, point_spans, regions) of the last nli call."""
         p, ps, r = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
-        _abi.check(_abi.lib.isrs_egn_work(self._h, ctypes.byref(p), ctypes.byref(ps), ctypes.byref(r)))
+        _abi.check(_abi.get().isrs_egn_work(self._h, ctypes.byref(p), ctypes.byref(ps), ctypes.byref(r)))
         return p.value, ps.value, r.value
 
+    def last_kernel_ms(self):
+        """([ms_D_only, ms_coherent, ms_reduce], [point_spans_D_only, point_spans_coherent, total])."""
+        ms = (ctypes.c_double * 3)()
+        ps = (ctypes.c_double * 3)()
+        _abi.check(_abi.get().isrs_egn_last_kernel_ms(self._h, ms, ps))
+        return list(ms), list(ps)
+
     def last_launch_count(self):
-        return _abi.lib.isrs_egn_last_launch_count(self._h)
+        return _abi.get().isrs_egn_last_launch_count(self._h)
 
     def close(self):
         if getattr(self, "_h", None):
-            _abi.lib.isrs_egn_destroy(self._h)
+            _abi.get().isrs_egn_destroy(self._h)
             self._h = None
 
     def __enter__(self):
@@ -115,7 +127,7 @@ def eta_host(link, coi=None, grid_n=None, delta_z_m=None, device=0, precision=64
         nco, cp = len(c), c.ctypes.data_as(_abi._ip)
     eta = np.zeros(nco)
     tt = np.zeros((nco, 5)) if terms else None
-    _abi.check(_abi.lib.isrs_egn_eta_host(ctypes.byref(pa.struct), ctypes.byref(n), device, nco, cp,
+    _abi.check(_abi.get().isrs_egn_eta_host(ctypes.byref(pa.struct), ctypes.byref(n), device, nco, cp,
                                           eta.ctypes.data_as(_abi._dp),
                                           tt.ctypes.data_as(_abi._dp) if terms else _abi._dp()))
     return (eta, tt) if terms else eta

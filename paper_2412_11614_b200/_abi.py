@@ -10,14 +10,15 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libisrs_egn.so")
+LIB_PATH = os.environ.get("ISRS_EGN_LIB") or os.path.join(_HERE, "libisrs_egn.so")
 
 OK, EINVAL, EOVERLAP, ERANGE, ENOMEM, ECUDA, EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
 MU_SEGMENT, MU_MACLAURIN = 0, 1
 FLAG_UNIT_LINK = 1
 
 EXPORTED = ("isrs_egn_create", "isrs_egn_nli", "isrs_egn_region_partials", "isrs_egn_work",
-            "isrs_egn_eta_host", "isrs_egn_last_launch_count", "isrs_egn_destroy",
+            "isrs_egn_eta_host", "isrs_egn_last_kernel_ms", "isrs_egn_last_launch_count",
+            "isrs_egn_destroy",
             "isrs_egn_strerror", "isrs_egn_last_error")
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -63,6 +64,8 @@ def _load():
     lib.isrs_egn_eta_host.argtypes = [ctypes.POINTER(Problem), ctypes.POINTER(Numerics), ctypes.c_int,
                                       ctypes.c_int32, _ip, _dp, _dp]
     lib.isrs_egn_eta_host.restype = ctypes.c_int
+    lib.isrs_egn_last_kernel_ms.argtypes = [ctypes.c_void_p, _dp, _dp]
+    lib.isrs_egn_last_kernel_ms.restype = ctypes.c_int
     lib.isrs_egn_last_launch_count.argtypes = [ctypes.c_void_p]
     lib.isrs_egn_last_launch_count.restype = ctypes.c_int
     lib.isrs_egn_destroy.argtypes = [ctypes.c_void_p]
@@ -74,12 +77,20 @@ def _load():
     return lib
 
 
-lib = _load()
+_LIB = None
+
+
+def get():
+    """The loaded libisrs_egn.so (loaded on first use; raises ImportError if it is not built)."""
+    global _LIB
+    if _LIB is None:
+        _LIB = _load()
+    return _LIB
 
 
 def check(rc):
     if rc != OK:
-        raise IsrsEgnError(rc, lib.isrs_egn_last_error().decode())
+        raise IsrsEgnError(rc, get().isrs_egn_last_error().decode())
     return rc
 
 

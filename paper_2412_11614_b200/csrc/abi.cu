@@ -92,6 +92,12 @@ struct isrs_egn {
   cudaStream_t last_stream = nullptr;
   bool have_result = false;
   int last_launches = 0;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool launched[2] = {false, false};
+  ~isrs_egn() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
 };
 
 static bool is_fin(double x) { return std::isfinite(x); }
@@ -354,14 +360,24 @@ extern "C" int isrs_egn_nli(isrs_egn_t* h, int32_t n_coi, const int32_t* coi, do
   kp.desc = h->d_desc.p; kp.partials = h->d_partials.p;
   kp.mode = (h->num.flags & ISRS_EGN_FLAG_UNIT_LINK) ? MODE_UNIT
             : (h->num.mu_mode == ISRS_EGN_MU_MACLAURIN ? MODE_MACLAURIN : MODE_SEGMENT);
+  if (!h->ev[0]) {
+    for (auto& e : h->ev)
+      if (cudaEventCreate(&e) != cudaSuccess) return cuda_fail(cudaGetLastError(), "cudaEventCreate");
+  }
   int launches = 0;
+  cudaEventRecord(h->ev[0], st);
   if (launch_integrand(kp, h->d_list_d.p, (long long)h->wl.list_d.size(), false, st, &launches) != 0)
     return cuda_fail(cudaGetLastError(), "integrand launch (D-only regions)");
+  cudaEventRecord(h->ev[1], st);
   if (launch_integrand(kp, h->d_list_c.p, (long long)h->wl.list_c.size(), true, st, &launches) != 0)
     return cuda_fail(cudaGetLastError(), "integrand launch (coherent regions)");
+  cudaEventRecord(h->ev[2], st);
+  h->launched[0] = !h->wl.list_d.empty();
+  h->launched[1] = !h->wl.list_c.empty();
   RParams rp{h->d_desc.p, h->d_partials.p, h->d_coi_off.p, h->d_coi.p, h->d_G.p, h->d_R.p,
              h->d_P.p, h->d_phi.p, h->d_psi.p, (int)c.size(), eta_dev, terms_dev, h->d_npts.p};
   if (launch_reduce(rp, st) != 0) return cuda_fail(cudaGetLastError(), "reduce launch");
+  cudaEventRecord(h->ev[3], st);
   launches += 1;
   h->last_launches = launches;
   h->last_stream = st;
@@ -408,6 +424,32 @@ extern "C" int isrs_egn_work(isrs_egn_t* h, int64_t* points, int64_t* point_span
   if (points) *points = tot;
   if (point_spans) *point_spans = tot * h->n_span;
   if (regions) *regions = (long long)h->wl.desc.size();
+  return ISRS_EGN_OK;
+}
+
+extern "C" int isrs_egn_last_kernel_ms(isrs_egn_t* h, double* ms_out, double* point_spans_out) {
+  if (!h || !ms_out) return fail(ISRS_EGN_EINVAL, "bad argument");
+  if (!h->have_result) return fail(ISRS_EGN_EINVAL, "no isrs_egn_nli() result yet");
+  cudaError_t ce = cudaEventSynchronize(h->ev[3]);
+  if (ce != cudaSuccess) return cuda_fail(ce, "event sync");
+  for (int k = 0; k < 3; ++k) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->ev[k], h->ev[k + 1]);
+    ms_out[k] = (k < 2 && !h->launched[k]) ? 0.0 : (double)ms;
+  }
+  if (point_spans_out) {
+    const size_t nr = h->wl.desc.size();
+    std::vector<double> np(nr);
+    ce = cudaMemcpy2D(np.data(), sizeof(double), h->d_partials.p + 5, 6 * sizeof(double),
+                      sizeof(double), nr, cudaMemcpyDeviceToHost);
+    if (ce != cudaSuccess) return cuda_fail(ce, "npts copy");
+    double a = 0, b = 0;
+    for (int id : h->wl.list_d) a += np[id];
+    for (int id : h->wl.list_c) b += np[id];
+    point_spans_out[0] = a * h->n_span;
+    point_spans_out[1] = b * h->n_span;
+    point_spans_out[2] = (a + b) * h->n_span;
+  }
   return ISRS_EGN_OK;
 }
 

@@ -5,8 +5,18 @@
 
 namespace isrs {
 
-constexpr int BLOCK = 256;          // threads per CTA (8 warps)
-constexpr int PPT = 4;              // grid points per thread in flight (independent Goertzel chains)
+#ifndef ISRS_BLOCK
+#define ISRS_BLOCK 256
+#endif
+#ifndef ISRS_PPT
+#define ISRS_PPT 4
+#endif
+#ifndef ISRS_MINB
+#define ISRS_MINB 2
+#endif
+constexpr int BLOCK = ISRS_BLOCK;   // threads per CTA (8 warps)
+constexpr int PPT = ISRS_PPT;       // grid points per thread in flight (independent Goertzel chains)
+constexpr int MIN_BLOCKS = ISRS_MINB;  // __launch_bounds__ min CTAs per SM
 constexpr int CP = BLOCK * PPT;     // points per chunk
 constexpr int LINE_CAP = 512;       // f3-lines compacted per segment (2N-1 <= 511 at N = 256)
 constexpr int TW_MAX = 64;          // envelope-table rows (f3-lines) resident in smem

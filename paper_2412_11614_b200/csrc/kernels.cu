@@ -208,6 +208,54 @@ __device__ inline void line_gate(const KParams& p, double f3, int k1, int k2, do
   *wF = ff;
 }
 
+
+// sin(pi x), cos(pi x): exact reduction to r = x - q/2 in [-1/4, 1/4] (q = rint(2x)), Taylor
+// polynomials in r^2 accurate to ~1 ulp on that interval, quadrant fix-up by selects and
+// sign-bit flips.  Branch-free so the PPT independent evaluations interleave (the library
+// sincospi() is ~2x the issue slots here because of its special-case branches).
+__device__ __forceinline__ void sincospi_d(double x, double* sp, double* cp) {
+  const double q = rint(x + x);
+  const double r = fma(q, -0.5, x);
+  const double r2 = r * r;
+  double ps = 7.952054001475508e-07;
+  ps = fma(ps, r2, -2.1915353447830204e-05);
+  ps = fma(ps, r2, 0.00046630280576761234);
+  ps = fma(ps, r2, -0.007370430945714348);
+  ps = fma(ps, r2, 0.08214588661112819);
+  ps = fma(ps, r2, -0.5992645293207919);
+  ps = fma(ps, r2, 2.550164039877345);
+  ps = fma(ps, r2, -5.167712780049969);
+  ps = fma(ps, r2, 3.141592653589793);
+  double pc = -1.387895246221376e-07;
+  pc = fma(pc, r2, 4.303069587032944e-06);
+  pc = fma(pc, r2, -0.00010463810492484565);
+  pc = fma(pc, r2, 0.001929574309403922);
+  pc = fma(pc, r2, -0.02580689139001405);
+  pc = fma(pc, r2, 0.23533063035889312);
+  pc = fma(pc, r2, -1.3352627688545893);
+  pc = fma(pc, r2, 4.058712126416768);
+  pc = fma(pc, r2, -4.934802200544679);
+  pc = fma(pc, r2, 1.0);
+  const double sr = r * ps;
+  const int n = (int)(__double2ll_rn(q) & 3);
+  double so = (n & 1) ? pc : sr;
+  double co = (n & 1) ? sr : pc;
+  const int sgn_s = (n & 2) ? (int)0x80000000 : 0;
+  const int sgn_c = ((n + 1) & 2) ? (int)0x80000000 : 0;
+  *sp = __hiloint2double(__double2hiint(so) ^ sgn_s, __double2loint(so));
+  *cp = __hiloint2double(__double2hiint(co) ^ sgn_c, __double2loint(co));
+}
+
+// 1/d for d > 0 normal: hardware approximation + two Newton steps (full double precision).
+__device__ __forceinline__ double rcp_d(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+
 __device__ inline long long gcd_ll(long long a, long long b) {
   while (b) {
     long long t = a % b;
@@ -221,7 +269,7 @@ __device__ inline long long gcd_ll(long long a, long long b) {
 // integrand (rows a3-a6)
 
 template <bool COH, int MODE>
-__global__ void __launch_bounds__(BLOCK, 2)
+__global__ void __launch_bounds__(BLOCK, MIN_BLOCKS)
 integrand_kernel(const KParams p, const int* __restrict__ list) {
   extern __shared__ __align__(16) char smem_raw[];
   Smem sm;
@@ -386,7 +434,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
 #pragma unroll
           for (int q = 0; q < PPT; ++q) {
             x[q] = uv[q] * fma(A3, Ssum[q], A2);     // chi h / pi  (Eq. 5 times h / pi)
-            sincospi(x[q], &sn[q], &cs[q]);          // z = e^{i chi h}
+            sincospi_d(x[q], &sn[q], &cs[q]);        // z = e^{i chi h}
           }
           double accr[PPT], acci[PPT];
           if (MODE == MODE_SEGMENT) {
@@ -402,22 +450,33 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
               rowp[q] = (const double2*)(sm.T + (li[q] - tb) * p.tstride);
             }
             const int npair = Kp >> 1;
+            // software-pipelined: the 16-byte loads of pair i2+1 are in flight while the PPT
+            // independent recurrences of pair i2 run interleaved (LDS latency ~29 cycles)
+            double2 tc[PPT];
+#pragma unroll
+            for (int q = 0; q < PPT; ++q) tc[q] = rowp[q][0];
+#pragma unroll 2
             for (int i2 = 0; i2 < npair - 1; ++i2) {
+              double2 tn[PPT];
+#pragma unroll
+              for (int q = 0; q < PPT; ++q) tn[q] = rowp[q][i2 + 1];
+              double n0[PPT];
+#pragma unroll
+              for (int q = 0; q < PPT; ++q) n0[q] = fma(c2[q], b1[q], tc[q].x - b2[q]);
 #pragma unroll
               for (int q = 0; q < PPT; ++q) {
-                const double2 t = rowp[q][i2];
-                const double n0 = fma(c2[q], b1[q], t.x - b2[q]);
-                const double n1 = fma(c2[q], n0, t.y - b1[q]);
-                b2[q] = n0;
+                const double n1 = fma(c2[q], n0[q], tc[q].y - b1[q]);
+                b2[q] = n0[q];
                 b1[q] = n1;
               }
+#pragma unroll
+              for (int q = 0; q < PPT; ++q) tc[q] = tn[q];
             }
 #pragma unroll
             for (int q = 0; q < PPT; ++q) {
-              const double2 t = rowp[q][npair - 1];
-              const double n0 = fma(c2[q], b1[q], t.x - b2[q]);   // b_1
+              const double n0 = fma(c2[q], b1[q], tc[q].x - b2[q]);   // b_1
               // sum_k a'_k z^k = a'_0 + z b_1 - b_2
-              accr[q] = fma(cs[q], n0, t.y - b1[q]);
+              accr[q] = fma(cs[q], n0, tc[q].y - b1[q]);
               acci[q] = sn[q] * n0;
             }
           }
@@ -428,7 +487,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
             if (MODE == MODE_SEGMENT) {
               // I_0 = (w - 1)/(i chi - alpha) = h (w - 1) conj(d) / |d|^2, d = -alpha h + i chi h
               const double wr1 = fma(Eh, cs[q], -1.0), wi = Eh * sn[q];
-              const double inv = gh / fma(px, px, ah * ah);     // gamma_s h / |d|^2
+              const double inv = gh * rcp_d(fma(px, px, ah * ah));   // gamma_s h / |d|^2
               const double nr = fma(wi, px, -ah * wr1);
               const double ni = -fma(px, wr1, ah * wi);
               mr = (nr * accr[q] - ni * acci[q]) * inv;
@@ -438,7 +497,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
               const double aL = __ldg(p.aL + s);
               const double xl = x[q] * Ks;        // chi L / pi
               double sl, cl;
-              sincospi(xl, &sl, &cl);
+              sincospi_d(xl, &sl, &cl);
               const double e1 = exp(-aL), e2 = e1 * e1;
               // eta / h = (e1 cis(chi L) - 1) / ((i chi - alpha) h): multiply by conj(d) / |d|^2
               const double ar = -ah, ai = px;     // d = (i chi - alpha) h
@@ -458,7 +517,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
             }
             // Y += gamma_s mu_s e^{i theta_s}, theta_s = pi * th (reading C3)
             double ps, pc;
-            sincospi(th[q], &ps, &pc);
+            sincospi_d(th[q], &ps, &pc);
             yr[q] = fma(mr, pc, fma(-mi, ps, yr[q]));
             yi[q] = fma(mr, ps, fma(mi, pc, yi[q]));
             double t2 = fma(x[q], (double)Ks, th[q]);   // theta_{s+1} = theta_s + chi_s L_s

@@ -28,7 +28,7 @@ def test_header_declares_the_boundary():
     syms = declared_symbols()
     for s in ("isrs_egn_create", "isrs_egn_nli", "isrs_egn_destroy"):
         assert s in syms
-    assert len(syms) == 9
+    assert len(syms) == 10
 
 
 def test_library_exports_every_declared_symbol(abi):
@@ -46,8 +46,8 @@ def test_library_is_sm100a_only(abi):
 
 
 def test_strerror(abi):
-    assert abi.lib.isrs_egn_strerror(0) == b"ok"
-    assert abi.lib.isrs_egn_strerror(-2) == b"channel bands overlap"
+    assert abi.get().isrs_egn_strerror(0) == b"ok"
+    assert abi.get().isrs_egn_strerror(-2) == b"channel bands overlap"
 
 
 def _create(abi, link, **kw):
@@ -55,8 +55,8 @@ def _create(abi, link, **kw):
     n = abi.numerics(kw.get("grid_n", link.grid_n), kw.get("dz", 1000.0), kw.get("precision", 64),
                      kw.get("mu_mode", 0))
     h = ctypes.c_void_p()
-    rc = abi.lib.isrs_egn_create(ctypes.byref(pa.struct), ctypes.byref(n), 0, ctypes.byref(h))
-    return rc, abi.lib.isrs_egn_last_error().decode(), h
+    rc = abi.get().isrs_egn_create(ctypes.byref(pa.struct), ctypes.byref(n), 0, ctypes.byref(h))
+    return rc, abi.get().isrs_egn_last_error().decode(), h
 
 
 def test_validation_errors_before_any_cuda(abi):
@@ -86,7 +86,7 @@ def test_validation_errors_before_any_cuda(abi):
 
 
 def test_destroy_null_safe(abi):
-    abi.lib.isrs_egn_destroy(None)
+    abi.get().isrs_egn_destroy(None)
 
 
 def test_product_never_imports_oracle():

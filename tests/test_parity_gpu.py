@@ -137,28 +137,30 @@ def sampled_regions(n, kappas):
 
 
 FULL = {
-    "c2": (None, (0, 19)),
-    "c3": (None, (50,)),
-    "c4": (None, (7, 41)),
-    "c5": ([0, 100, 199], (100, 199)),
+    "c2": (None, sampled_regions(40, (0, 19))),
+    "c3": (None, sampled_regions(100, (50,))),
+    "c4": (None, sampled_regions(80, (7, 41))),
+    "c5": ([0, 100, 199], [(100, 100, 100), (100, 103, 98), (199, 199, 198), (0, 40, 0)]),
 }
 
 
 @pytest.mark.parametrize("cfg", sorted(FULL))
 def test_full_size_region_parity(isrs, cfg):
     link = bj_config(cfg)
-    coi, kappas = FULL[cfg]
+    coi, regs = FULL[cfg]
     with isrs.Engine(link) as e:
         eta = e.nli(coi=coi)
         torch.cuda.synchronize()
         eta = eta.cpu().numpy()
         assert np.all(np.isfinite(eta)) and np.all(eta > 0)
-        regs = sampled_regions(link.n_ch, kappas)
         got = e.region_partials(regs)
         pts, pspans, nreg = e.work()
     assert pspans == pts * link.n_span and nreg > 0
     for (kappa, k1, k2), g in zip(regs, got):
         want, npts = egn.region_partials(link, kappa, k1, k2)
+        if npts == 0:      # empty region: either not listed (-1) or listed with no support
+            assert g[5] in (0, -1) and np.all(g[:5] == 0.0) and np.all(want == 0.0)
+            continue
         assert g[5] == npts, (cfg, kappa, k1, k2)
         tol = max(TOL_ETA, 64 * EPS * theta_max(link, kappa, k1, k2))
         scale = max(np.max(np.abs(want)), 1e-300)
