@@ -243,7 +243,7 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
   int kpad = (kmax + 1) & ~1;
   h->kstride = kpad;
   h->tstride = kpad + 2;
-  const size_t t_budget = 48 * 1024;
+  const size_t t_budget = T_BYTES;
   h->tw = (int)std::min<size_t>(TW_MAX, t_budget / ((size_t)h->tstride * 8));
   if (h->tw < 2) {
     delete h;

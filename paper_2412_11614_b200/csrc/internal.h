@@ -6,20 +6,29 @@
 namespace isrs {
 
 #ifndef ISRS_BLOCK
-#define ISRS_BLOCK 256
+#define ISRS_BLOCK 128
 #endif
 #ifndef ISRS_PPT
 #define ISRS_PPT 4
 #endif
 #ifndef ISRS_MINB
-#define ISRS_MINB 2
+#define ISRS_MINB 4
 #endif
-constexpr int BLOCK = ISRS_BLOCK;   // threads per CTA (8 warps)
+constexpr int BLOCK = ISRS_BLOCK;   // threads per CTA (4 warps; 4 CTAs per SM)
 constexpr int PPT = ISRS_PPT;       // grid points per thread in flight (independent Goertzel chains)
 constexpr int MIN_BLOCKS = ISRS_MINB;  // __launch_bounds__ min CTAs per SM
 constexpr int CP = BLOCK * PPT;     // points per chunk
 constexpr int LINE_CAP = 512;       // f3-lines compacted per segment (2N-1 <= 511 at N = 256)
-constexpr int TW_MAX = 64;          // envelope-table rows (f3-lines) resident in smem
+#ifndef ISRS_TW
+#define ISRS_TW 64
+#endif
+#ifndef ISRS_TBYTES
+#define ISRS_TBYTES (24 * 1024)
+#endif
+constexpr int TW_MAX = ISRS_TW;     // envelope-table rows (f3-lines) resident in smem
+constexpr int T_BYTES = ISRS_TBYTES;  // smem budget of the envelope table
+constexpr int LPT = LINE_CAP / BLOCK;  // lattice lines scanned per thread
+static_assert(LINE_CAP % BLOCK == 0, "LINE_CAP must be a multiple of BLOCK");
 
 // region flags (reading C8: a term whose gate or weight is zero is not evaluated)
 enum : int { NEED_E = 1, NEED_F = 2, NEED_G = 4, NEED_H = 8 };

@@ -309,13 +309,13 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
 
   for (int seg0 = 0; seg0 < J; seg0 += LINE_CAP) {
     const int nl = min(LINE_CAP, J - seg0);
-    // ---- line scan: each thread owns two consecutive lines (order-preserving compaction)
-    int cnt[2], first[2];
-    double lwD[2], lwE[2], lwF[2];
+    // ---- line scan: each thread owns LPT consecutive lines (order-preserving compaction)
+    int cnt[LPT], first[LPT];
+    double lwD[LPT], lwE[LPT], lwF[LPT];
     int2 v = make_int2(0, 0);
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int jl = 2 * tid + q;
+    for (int q = 0; q < LPT; ++q) {
+      const int jl = LPT * tid + q;
       cnt[q] = 0;
       first[q] = 0;
       lwD[q] = lwE[q] = lwF[q] = 0.0;
@@ -346,9 +346,9 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
     int2 tot;
     int2 pos = block_scan2(v, sm.scan, &tot);
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < LPT; ++q) {
       if (cnt[q] > 0) {
-        sm.sl_j[pos.x] = seg0 + 2 * tid + q;
+        sm.sl_j[pos.x] = seg0 + LPT * tid + q;
         sm.sl_first[pos.x] = first[q];
         sm.sl_start[pos.x] = pos.y;
         sm.wD[pos.x] = lwD[q];
