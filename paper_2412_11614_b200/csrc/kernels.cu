@@ -67,7 +67,8 @@ struct Smem {
   double* T;         // [tw][tstride] reversed envelope rows: T[row][i] = a'_{Kp-1-i}(f3_row)
   int* sl_j;         // [LINE_CAP] compacted supported line index j
   int* sl_first;     // [LINE_CAP] first m1 on the line
-  int* sl_start;     // [LINE_CAP+1] exclusive prefix of point counts
+  int* sl_start;     // [LINE_CAP+1] exclusive prefix of point counts padded to multiples of PPT
+  int* sl_cnt;       // [LINE_CAP] points on the line (unpadded)
   double* wD;        // [LINE_CAP] sum_t t G_k3         (D, G weights)
   double* wE;        // [LINE_CAP] sum_t t [k3 == k1]   (E, H weights)
   int* scan;         // [BLOCK] scan scratch (int2)
@@ -93,10 +94,11 @@ __host__ __device__ inline size_t smem_layout(int tstride, int tw, int N, bool c
   size_t oJ = take(sizeof(int) * LINE_CAP);
   size_t oF = take(sizeof(int) * LINE_CAP);
   size_t oS = take(sizeof(int) * (LINE_CAP + 1));
+  size_t oN = take(sizeof(int) * LINE_CAP);
   size_t oD = take(sizeof(double) * LINE_CAP);
   size_t oE = take(sizeof(double) * LINE_CAP);
   size_t oW = take(sizeof(double) * LINE_CAP);
-  size_t oC = take(sizeof(int) * 2 * BLOCK);
+  size_t oC = take(sizeof(int4) * (BLOCK / 32 + 1));
   size_t oR = take(sizeof(double) * BLOCK);
   size_t oY = 0, oRow = 0, oCol = 0, oLine = 0;
   if (coh) {
@@ -110,6 +112,7 @@ __host__ __device__ inline size_t smem_layout(int tstride, int tw, int N, bool c
     s->sl_j = (int*)(base + oJ);
     s->sl_first = (int*)(base + oF);
     s->sl_start = (int*)(base + oS);
+    s->sl_cnt = (int*)(base + oN);
     s->wD = (double*)(base + oD);
     s->wE = (double*)(base + oE);
     s->wF = (double*)(base + oW);
@@ -127,35 +130,37 @@ size_t integrand_smem_bytes(int tstride, int tw, int N, bool coherent) {
   return smem_layout(tstride, tw, N, coherent, nullptr, nullptr);
 }
 
-// Block-wide exclusive scan of an int pair; returns totals.  All threads must call.
-__device__ inline int2 block_scan2(int2 v, int* scratch, int2* total) {
+// Block-wide exclusive scan of an int triple (w unused); returns totals.  All threads must call.
+__device__ inline int4 block_scan3(int4 v, int* scratch, int4* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int2 x = v;
+  int4 x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    int a = __shfl_up_sync(0xffffffffu, x.x, o);
-    int b = __shfl_up_sync(0xffffffffu, x.y, o);
-    if (lane >= o) { x.x += a; x.y += b; }
+    const int a = __shfl_up_sync(0xffffffffu, x.x, o);
+    const int b = __shfl_up_sync(0xffffffffu, x.y, o);
+    const int c = __shfl_up_sync(0xffffffffu, x.z, o);
+    if (lane >= o) { x.x += a; x.y += b; x.z += c; }
   }
-  int2* ws = (int2*)scratch;
+  int4* ws = (int4*)scratch;
   __syncthreads();
   if (lane == 31) ws[warp] = x;
   __syncthreads();
   if (warp == 0) {
-    int2 w = (lane < BLOCK / 32) ? ws[lane] : make_int2(0, 0);
+    int4 w = (lane < BLOCK / 32) ? ws[lane] : make_int4(0, 0, 0, 0);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int a = __shfl_up_sync(0xffffffffu, w.x, o);
-      int b = __shfl_up_sync(0xffffffffu, w.y, o);
-      if (lane >= o) { w.x += a; w.y += b; }
+      const int a = __shfl_up_sync(0xffffffffu, w.x, o);
+      const int b = __shfl_up_sync(0xffffffffu, w.y, o);
+      const int c = __shfl_up_sync(0xffffffffu, w.z, o);
+      if (lane >= o) { w.x += a; w.y += b; w.z += c; }
     }
     if (lane < BLOCK / 32) ws[lane] = w;   // inclusive warp prefix
   }
   __syncthreads();
-  int2 base = (warp > 0) ? ws[warp - 1] : make_int2(0, 0);
+  const int4 base = (warp > 0) ? ws[warp - 1] : make_int4(0, 0, 0, 0);
   *total = ws[BLOCK / 32 - 1];
   __syncthreads();
-  return make_int2(base.x + x.x - v.x, base.y + x.y - v.y);
+  return make_int4(base.x + x.x - v.x, base.y + x.y - v.y, base.z + x.z - v.z, 0);
 }
 
 // Fixed-tree block sum (deterministic).  All threads must call.
@@ -312,7 +317,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
     // ---- line scan: each thread owns LPT consecutive lines (order-preserving compaction)
     int cnt[LPT], first[LPT];
     double lwD[LPT], lwE[LPT], lwF[LPT];
-    int2 v = make_int2(0, 0);
+    int4 v = make_int4(0, 0, 0, 0);
 #pragma unroll
     for (int q = 0; q < LPT; ++q) {
       const int jl = LPT * tid + q;
@@ -338,24 +343,26 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
             cnt[q] = n;
             first[q] = fm;
             v.x += 1;
-            v.y += n;
+            v.y += (n + PPT - 1) / PPT * PPT;   // slots: each line padded to whole PPT-groups
+            v.z += n;
           }
         }
       }
     }
-    int2 tot;
-    int2 pos = block_scan2(v, sm.scan, &tot);
+    int4 tot;
+    int4 pos = block_scan3(v, sm.scan, &tot);
 #pragma unroll
     for (int q = 0; q < LPT; ++q) {
       if (cnt[q] > 0) {
         sm.sl_j[pos.x] = seg0 + LPT * tid + q;
         sm.sl_first[pos.x] = first[q];
         sm.sl_start[pos.x] = pos.y;
+        sm.sl_cnt[pos.x] = cnt[q];
         sm.wD[pos.x] = lwD[q];
         sm.wE[pos.x] = lwE[q];
         sm.wF[pos.x] = lwF[q];
         pos.x += 1;
-        pos.y += cnt[q];
+        pos.y += (cnt[q] + PPT - 1) / PPT * PPT;
       }
     }
     const int S = tot.x, NP = tot.y;
@@ -364,7 +371,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
       for (int i = tid; i < S; i += BLOCK) sm.lineacc[i] = make_double2(0.0, 0.0);
     }
     __syncthreads();
-    npts_total += NP;
+    npts_total += tot.z;
     if (NP == 0) continue;
 
     int tb = 0, tn = 0, tcls = -1;  // resident table: compacted lines [tb, tb + tn), class tcls
@@ -375,25 +382,27 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
       const int p_end = min(p0 + CP, sm.sl_start[lim]);
       const int i_last = line_of(sm.sl_start, S, p_end - 1);
 
-      // ---- per-thread points
-      int li[PPT];
+      // ---- per-thread points: PPT consecutive slots of one line (lines are padded to whole
+      // groups), so one envelope-table row serves all PPT recurrences of the thread
+      const int slot0 = p0 + PPT * tid;
+      const bool gvalid = slot0 < p_end;
+      const int li = gvalid ? line_of(sm.sl_start, S, slot0) : i_first;
+      const int lj = sm.sl_j[li];
+      const int kq0 = slot0 - sm.sl_start[li];
+      const int lcnt = sm.sl_cnt[li];
       bool valid[PPT];
-      double uv[PPT], Ssum[PPT], f3v[PPT];
+      double uv[PPT], Ssum[PPT];
+      const double f3l = __dadd_rn(C, g * (double)lj);
 #pragma unroll
       for (int q = 0; q < PPT; ++q) {
-        const int idx = p0 + q * BLOCK + tid;
-        valid[q] = idx < p_end;
-        const int i = valid[q] ? line_of(sm.sl_start, S, idx) : i_first;
-        li[q] = i;
-        const int j = sm.sl_j[i];
-        const int m1 = sm.sl_first[i] + b * (valid[q] ? idx - sm.sl_start[i] : 0);
-        const int m2 = (j - a * m1) / b;
+        valid[q] = gvalid && (kq0 + q < lcnt);
+        const int m1 = sm.sl_first[li] + b * (valid[q] ? kq0 + q : 0);
+        const int m2 = (lj - a * m1) / b;
         const double f1 = __dadd_rn(lo1, __dmul_rn((double)m1 + 0.5, d1));   // C6 bin centres
         const double f2 = __dadd_rn(lo2, __dmul_rn((double)m2 + 0.5, d2));
         const double u = __dadd_rn(f1, -f), w = __dadd_rn(f2, -f);
         uv[q] = __dmul_rn(u, w);
         Ssum[q] = __dadd_rn(f1, f2);
-        f3v[q] = __dadd_rn(C, g * (double)j);
       }
 
       double yr[PPT], yi[PPT], th[PPT];
@@ -441,42 +450,36 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
             // ---- Goertzel over the K_s segments (Eqs. 8-9 with I_k = I_0 w^k)
             const int Kp = (__ldg(p.Kc + cls) + 1) & ~1;
             double c2[PPT], b1[PPT], b2[PPT];
-            const double2* rowp[PPT];
 #pragma unroll
             for (int q = 0; q < PPT; ++q) {
               c2[q] = cs[q] + cs[q];
               b1[q] = 0.0;
               b2[q] = 0.0;
-              rowp[q] = (const double2*)(sm.T + (li[q] - tb) * p.tstride);
             }
+            const double2* rowp = (const double2*)(sm.T + (li - tb) * p.tstride);
             const int npair = Kp >> 1;
             // software-pipelined: the 16-byte loads of pair i2+1 are in flight while the PPT
             // independent recurrences of pair i2 run interleaved (LDS latency ~29 cycles)
-            double2 tc[PPT];
-#pragma unroll
-            for (int q = 0; q < PPT; ++q) tc[q] = rowp[q][0];
-#pragma unroll 2
+            double2 tc = rowp[0];
+#pragma unroll 4
             for (int i2 = 0; i2 < npair - 1; ++i2) {
-              double2 tn[PPT];
-#pragma unroll
-              for (int q = 0; q < PPT; ++q) tn[q] = rowp[q][i2 + 1];
+              const double2 tn = rowp[i2 + 1];
               double n0[PPT];
 #pragma unroll
-              for (int q = 0; q < PPT; ++q) n0[q] = fma(c2[q], b1[q], tc[q].x - b2[q]);
+              for (int q = 0; q < PPT; ++q) n0[q] = fma(c2[q], b1[q], tc.x - b2[q]);
 #pragma unroll
               for (int q = 0; q < PPT; ++q) {
-                const double n1 = fma(c2[q], n0[q], tc[q].y - b1[q]);
+                const double n1 = fma(c2[q], n0[q], tc.y - b1[q]);
                 b2[q] = n0[q];
                 b1[q] = n1;
               }
-#pragma unroll
-              for (int q = 0; q < PPT; ++q) tc[q] = tn[q];
+              tc = tn;
             }
 #pragma unroll
             for (int q = 0; q < PPT; ++q) {
-              const double n0 = fma(c2[q], b1[q], tc[q].x - b2[q]);   // b_1
+              const double n0 = fma(c2[q], b1[q], tc.x - b2[q]);   // b_1
               // sum_k a'_k z^k = a'_0 + z b_1 - b_2
-              accr[q] = fma(cs[q], n0, tc[q].y - b1[q]);
+              accr[q] = fma(cs[q], n0, tc.y - b1[q]);
               acci[q] = sn[q] * n0;
             }
           }
@@ -510,7 +513,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
               const double n2r = fma(e2, cl, -1.0), n2i = e2 * sl;
               const double et2_r = (n2r * br + n2i * ai) * den2;
               const double et2_i = (n2i * br - n2r * ai) * den2;
-              const double cf = __ldg(p.mac_c + s) * f3v[q];
+              const double cf = __ldg(p.mac_c + s) * f3l;
               // (values above are eta / h; gh = gamma h restores the scale)
               mr = (eta_r - cf * (eta_r - et2_r)) * gh;
               mi = (eta_i - cf * (eta_i - et2_i)) * gh;
@@ -529,18 +532,18 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
       // ---- D accumulation
 #pragma unroll
       for (int q = 0; q < PPT; ++q) {
-        if (valid[q]) Dacc = fma(sm.wD[li[q]], fma(yr[q], yr[q], yi[q] * yi[q]), Dacc);
+        if (valid[q]) Dacc = fma(sm.wD[li], fma(yr[q], yr[q], yi[q] * yi[q]), Dacc);
       }
 
       if (COH) {
 #pragma unroll
         for (int q = 0; q < PPT; ++q)
-          sm.ybuf[q * BLOCK + tid] = valid[q] ? make_double2(yr[q], yi[q]) : make_double2(0.0, 0.0);
+          sm.ybuf[PPT * tid + q] = valid[q] ? make_double2(yr[q], yi[q]) : make_double2(0.0, 0.0);
         __syncthreads();
         // lines (G, H): one thread per line in the chunk, points in order
         if (flags & (NEED_G | NEED_H)) {
           for (int i = i_first + tid; i <= i_last; i += BLOCK) {
-            const int s0 = max(sm.sl_start[i], p0), s1 = min(sm.sl_start[i + 1], p_end);
+            const int s0 = max(sm.sl_start[i], p0), s1 = min(sm.sl_start[i] + sm.sl_cnt[i], p_end);
             double2 acc = sm.lineacc[i];
             for (int t = s0; t < s1; ++t) {
               const double2 y = sm.ybuf[t - p0];
