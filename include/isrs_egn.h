@@ -67,7 +67,10 @@ typedef struct {
 enum { ISRS_EGN_MU_SEGMENT = 0,    /* Eqs. 8-10 (default, the hot path)                       */
        ISRS_EGN_MU_MACLAURIN = 1   /* Eq. 4 (NEXT-1)                                          */ };
 
-enum { ISRS_EGN_FLAG_UNIT_LINK = 1u /* test hook: Y := 1 (oracle pin P6)                     */ };
+enum { ISRS_EGN_FLAG_UNIT_LINK = 1u, /* test hook: Y := 1 (oracle pin P6)                    */
+       ISRS_EGN_FLAG_NO_CHAIN = 2u   /* evaluate every span's segment sum (Eq. 8) on its own
+                                        instead of chaining runs of identical consecutive spans
+                                        into one recurrence (R9); same sum, A/B hook */ };
 
 typedef struct {
   int32_t grid_n;      /* N: N x N bin-centre grid per (kappa1, kappa2) region; even, >= 2 (C6) */

@@ -13,10 +13,10 @@ import ctypes
 import numpy as np
 
 from . import _abi
-from ._abi import (FLAG_UNIT_LINK, MU_MACLAURIN, MU_SEGMENT, IsrsEgnError, ProblemArrays,  # noqa: F401
+from ._abi import (FLAG_NO_CHAIN, FLAG_UNIT_LINK, MU_MACLAURIN, MU_SEGMENT, IsrsEgnError, ProblemArrays,  # noqa: F401
                    numerics)
 
-__all__ = ["Engine", "eta_host", "IsrsEgnError", "MU_SEGMENT", "MU_MACLAURIN", "FLAG_UNIT_LINK",
+__all__ = ["Engine", "eta_host", "IsrsEgnError", "MU_SEGMENT", "MU_MACLAURIN", "FLAG_UNIT_LINK", "FLAG_NO_CHAIN",
            "library_path"]
 
 

@@ -79,7 +79,8 @@ struct isrs_egn {
   DevBuf<double> d_lo, d_hi, d_f, d_G, d_R, d_P, d_phi, d_psi, d_delta;
   DevBuf<long long> d_rate;
   DevBuf<double> d_A2, d_A3, d_Eh, d_ah, d_gh, d_macc, d_aL;
-  DevBuf<int> d_K, d_cls, d_Kc;
+  DevBuf<int> d_K, d_cls, d_Kc, d_chain_s0, d_chain_g;
+  int n_chain = 0;
   DevBuf<double> d_lnA, d_zeta;
   int kstride = 0, tstride = 0, tw = 0;
   // work list cache (last call)
@@ -239,6 +240,28 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
     aL.push_back(a * L);
   }
   h->n_cls = (int)cL.size();
+  // ---- span chains (reading R9): identical consecutive spans (same L, alpha, beta2, beta3,
+  // gamma, C_r, hence the same z = e^{i chi h} and envelope table) with an even K_s share one
+  // recurrence over G * K_s segments, G * K_s <= CHAIN_MAX.  Segment mode only.
+  std::vector<int> ch_s0, ch_g;
+  const bool chain_ok = num.mu_mode == ISRS_EGN_MU_SEGMENT &&
+                        !(num.flags & (ISRS_EGN_FLAG_NO_CHAIN | ISRS_EGN_FLAG_UNIT_LINK));
+  for (int s = 0; s < p->n_span; ++s) {
+    const bool same = s > 0 && chain_ok && (K[s] % 2 == 0) && p->length_m[s] == p->length_m[s - 1] &&
+                      p->alpha_per_m[s] == p->alpha_per_m[s - 1] &&
+                      p->beta2_s2_per_m[s] == p->beta2_s2_per_m[s - 1] &&
+                      p->beta3_s3_per_m[s] == p->beta3_s3_per_m[s - 1] &&
+                      p->gamma_per_w_m[s] == p->gamma_per_w_m[s - 1] &&
+                      p->cr_per_w_m_hz[s] == p->cr_per_w_m_hz[s - 1] &&
+                      (long long)(ch_g.back() + 1) * K[s] <= CHAIN_MAX;
+    if (same) {
+      ch_g.back() += 1;
+    } else {
+      ch_s0.push_back(s);
+      ch_g.push_back(1);
+    }
+  }
+  h->n_chain = (int)ch_s0.size();
   int kmax = *std::max_element(cK.begin(), cK.end());
   int kpad = (kmax + 1) & ~1;
   h->kstride = kpad;
@@ -260,7 +283,7 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
             h->d_rate.upload(h->rate) && h->d_A2.upload(A2) && h->d_A3.upload(A3) &&
             h->d_Eh.upload(Eh) && h->d_ah.upload(ah) && h->d_gh.upload(gh) &&
             h->d_macc.upload(macc) && h->d_aL.upload(aL) && h->d_K.upload(K) && h->d_cls.upload(cls) &&
-            h->d_Kc.upload(cK);
+            h->d_Kc.upload(cK) && h->d_chain_s0.upload(ch_s0) && h->d_chain_g.upload(ch_g);
   DevBuf<double> dL, dA, dC;
   ok = ok && dL.upload(cL) && dA.upload(cA) && dC.upload(cC) &&
        h->d_lnA.alloc((size_t)h->n_cls * h->kstride) && h->d_zeta.alloc((size_t)h->n_cls * h->kstride);
@@ -355,6 +378,7 @@ extern "C" int isrs_egn_nli(isrs_egn_t* h, int32_t n_coi, const int32_t* coi, do
   kp.A2 = h->d_A2.p; kp.A3 = h->d_A3.p; kp.Eh = h->d_Eh.p; kp.ah = h->d_ah.p; kp.gh = h->d_gh.p;
   kp.mac_c = h->d_macc.p; kp.aL = h->d_aL.p; kp.K = h->d_K.p; kp.cls = h->d_cls.p;
   kp.n_span = h->n_span;
+  kp.chain_s0 = h->d_chain_s0.p; kp.chain_g = h->d_chain_g.p; kp.n_chain = h->n_chain;
   kp.lnA = h->d_lnA.p; kp.zeta = h->d_zeta.p; kp.Kc = h->d_Kc.p; kp.n_cls = h->n_cls;
   kp.kstride = h->kstride; kp.tstride = h->tstride; kp.tw = h->tw; kp.N = h->N;
   kp.desc = h->d_desc.p; kp.partials = h->d_partials.p;

@@ -28,6 +28,12 @@ constexpr int LINE_CAP = 512;       // f3-lines compacted per segment (2N-1 <= 5
 constexpr int TW_MAX = ISRS_TW;     // envelope-table rows (f3-lines) resident in smem
 constexpr int T_BYTES = ISRS_TBYTES;  // smem budget of the envelope table
 constexpr int LPT = LINE_CAP / BLOCK;  // lattice lines scanned per thread
+#ifndef ISRS_CHAIN_MAX
+#define ISRS_CHAIN_MAX 400
+#endif
+// longest chained recurrence (segments): the phase of the implicit z^n drifts by <= n^2 eps
+// (fl(2 cos(chi h)) is exact to eps), 400^2 * 1.1e-16 = 1.8e-11 relative per point (DESIGN R9)
+constexpr int CHAIN_MAX = ISRS_CHAIN_MAX;
 static_assert(LINE_CAP % BLOCK == 0, "LINE_CAP must be a multiple of BLOCK");
 
 // region flags (reading C8: a term whose gate or weight is zero is not evaluated)
@@ -64,6 +70,11 @@ struct KParams {
   const int* K;         // segments K_s = ceil(L/dz)
   const int* cls;       // span class (spans sharing L, alpha, C_r share envelope tables)
   int n_span;
+  // span chains (reading R9): runs of identical consecutive spans whose segment sums are
+  // evaluated as ONE recurrence over G*K segments; chain c covers spans [s0[c], s0[c] + g[c])
+  const int* chain_s0;
+  const int* chain_g;
+  int n_chain;
   // span classes: envelope a'_k(f3) = exp(lnA[c][k] - zeta[c][k] f3)
   const double* lnA;    // [n_cls][kstride]  ln(c_k) - alpha h k
   const double* zeta;   // [n_cls][kstride]

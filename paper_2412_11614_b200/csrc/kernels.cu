@@ -414,7 +414,9 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
       }
 
       if (MODE != MODE_UNIT) {
-        for (int s = 0; s < p.n_span; ++s) {
+        for (int ch = 0; ch < p.n_chain; ++ch) {
+          // chain of G identical consecutive spans starting at s (G = 1 unless chained, R9)
+          const int s = __ldg(p.chain_s0 + ch), G = __ldg(p.chain_g + ch);
           const int cls = __ldg(p.cls + s);
           if (MODE == MODE_SEGMENT &&
               (cls != tcls || i_first < tb || i_last >= tb + tn)) {
@@ -431,8 +433,9 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
               const int row = e / Kp, ii = e - row * Kp;
               const int k = Kp - 1 - ii;
               const double f3 = __dadd_rn(C, g * (double)sm.sl_j[tb + row]);
-              sm.T[row * p.tstride + ii] =
-                  (k < Kc) ? exp(__ldg(lnA + k) - __ldg(zt + k) * f3) : 0.0;
+              const double v = (k < Kc) ? exp(__ldg(lnA + k) - __ldg(zt + k) * f3) : 0.0;
+              sm.T[row * p.tstride + ii] = v;
+              if (ii < 2) sm.T[row * p.tstride + Kp + ii] = v;   // wrap pair for span chains (R9)
             }
             __syncthreads();
           }
@@ -460,20 +463,25 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
             const int npair = Kp >> 1;
             // software-pipelined: the 16-byte loads of pair i2+1 are in flight while the PPT
             // independent recurrences of pair i2 run interleaved (LDS latency ~29 cycles)
+            // span chain (R9): the coefficients of G identical spans repeat with period K, so
+            // the row is walked G times (rowp[npair] holds a copy of rowp[0] for the wrap)
             double2 tc = rowp[0];
+            for (int gi = 0; gi < G; ++gi) {
+              const int nit = (gi == G - 1) ? npair - 1 : npair;
 #pragma unroll 4
-            for (int i2 = 0; i2 < npair - 1; ++i2) {
-              const double2 tn = rowp[i2 + 1];
-              double n0[PPT];
+              for (int i2 = 0; i2 < nit; ++i2) {
+                const double2 tn = rowp[i2 + 1];
+                double n0[PPT];
 #pragma unroll
-              for (int q = 0; q < PPT; ++q) n0[q] = fma(c2[q], b1[q], tc.x - b2[q]);
+                for (int q = 0; q < PPT; ++q) n0[q] = fma(c2[q], b1[q], tc.x - b2[q]);
 #pragma unroll
-              for (int q = 0; q < PPT; ++q) {
-                const double n1 = fma(c2[q], n0[q], tc.y - b1[q]);
-                b2[q] = n0[q];
-                b1[q] = n1;
+                for (int q = 0; q < PPT; ++q) {
+                  const double n1 = fma(c2[q], n0[q], tc.y - b1[q]);
+                  b2[q] = n0[q];
+                  b1[q] = n1;
+                }
+                tc = tn;
               }
-              tc = tn;
             }
 #pragma unroll
             for (int q = 0; q < PPT; ++q) {
@@ -523,7 +531,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
             sincospi_d(th[q], &ps, &pc);
             yr[q] = fma(mr, pc, fma(-mi, ps, yr[q]));
             yi[q] = fma(mr, ps, fma(mi, pc, yi[q]));
-            double t2 = fma(x[q], (double)Ks, th[q]);   // theta_{s+1} = theta_s + chi_s L_s
+            double t2 = fma(x[q], (double)(Ks * G), th[q]);   // theta += chi_s L_s (x G spans)
             th[q] = t2 - 2.0 * rint(0.5 * t2);          // exact reduction mod 2 (units of pi)
           }
         }

@@ -51,6 +51,8 @@ TINY = {
     "ragged_chunks_N34": dict(n_ch=2, rates_gbd=(68,), spacing_ghz=100.0, n_span=2, grid_n=34,
                               fmts=("64qam",), tilt_db=2.0),
     "single_channel_N64": dict(n_ch=1, rates_gbd=(64,), n_span=3, grid_n=64, fmts=("qpsk",)),
+    "long_link_chained": dict(n_ch=3, rates_gbd=(96,), spacing_ghz=100.0, n_span=23, grid_n=8,
+                              fmts=("16qam", "qpsk"), power_dbm=4.0),
     "strong_isrs": dict(n_ch=3, rates_gbd=(96,), spacing_ghz=100.0, n_span=2, grid_n=8,
                         cr_w_km_thz=5.0, power_dbm=12.0, fmts=("16qam",)),
 }
@@ -167,6 +169,17 @@ def test_full_size_region_parity(isrs, cfg):
         for t in range(5):
             assert abs(g[t] - want[t]) <= tol * max(abs(want[t]), 1e-300) or \
                 abs(g[t] - want[t]) <= 1e-13 * scale, (cfg, (kappa, k1, k2), t, g[t], want[t], tol)
+
+
+@pytest.mark.parametrize("cfg,coi", [("c2", [0, 19, 39]), ("c5", [100])])
+def test_span_chaining_matches_unchained(isrs, cfg, coi):
+    """R9: chaining identical consecutive spans into one recurrence is the same sum (Eqs. 8, 22);
+    it must agree with the per-span evaluation to the parity bar at full BASELINE sizes."""
+    link = bj_config(cfg)
+    a, ta = gpu_eta(isrs, link, coi=coi)
+    b, tb = gpu_eta(isrs, link, coi=coi, flags=isrs.FLAG_NO_CHAIN)
+    assert np.all(np.abs(a - b) / b <= TOL_ETA), (a, b, np.abs(a - b) / b)
+    assert np.all(np.abs(ta - tb) <= TOL_ETA * np.abs(tb).sum(axis=1, keepdims=True))
 
 
 def test_full_size_determinism_c2(isrs):

@@ -11,6 +11,10 @@ mkdir -p "$OUT"
 nvidia-smi > "$OUT/nvidia-smi.txt" 2>&1
 nproc > "$OUT/nproc.txt"; lscpu | head -20 >> "$OUT/nproc.txt"
 python -m paper_2412_11614_b200.build > "$OUT/build.log" 2>&1
+if [[ $STAGES == *p* ]]; then
+  for b in tools/dmma_probe tools/fp64_pipes; do [ -x $b ] && timeout 120 ./$b > "$OUT/$(basename $b).txt" 2>&1; done
+  echo "probes rc=$?" >> "$OUT/status"
+fi
 if [[ $STAGES == *t* ]]; then
   timeout 1200 python -m pytest tests -m gpu -x -q > "$OUT/pytest_gpu.log" 2>&1; echo "pytest rc=$?" >> "$OUT/status"
 fi
