@@ -38,13 +38,21 @@ def fp64_peak_tflops(mhz=SM_MAX_MHZ):
     return SMS * FP64_LANES * 2 * mhz * 1e6 / 1e12
 
 
-def algorithmic_flops_per_point(link):
-    """Per grid point summed over spans: 3 flops per segment of the second-order recurrence
-    (one DFMA + one DADD, Goertzel form of Eqs. 8-9) plus 40 flops of per-span arithmetic (chi,
-    I_0, mu, Y accumulation, phase); the two sincospi per span are not counted."""
-    K = np.ceil(np.asarray(link.length_m) / link.delta_z_m)
-    Kp = 2 * np.ceil(K / 2)
-    return float(np.sum(3 * (Kp - 1) + 40))
+def algorithmic_work_per_point(chain_g, k_s):
+    """Algorithmic FP64 work per grid point summed over the link, given the span
+    chains (reading R9): a chain of G spans with K segments (K_p = K rounded up to even) runs
+    one second-order recurrence over G*K_p segments, 1 DFMA + 1 DADD each = 3 flops / 2 FP64
+    pipe slots (the first step is a bare add: -3 / -2), plus 40 flops / 25 slots of per-chain
+    arithmetic (chi, 2cos, I_0, mu, Y accumulation, phase advance); the two sincospi and the
+    reciprocal seed per chain are not counted.  Returns (flops, fp64 pipe slots)."""
+    flops = slots = 0.0
+    s = 0
+    for g in chain_g:
+        kp = 2 * ((int(k_s[s]) + 1) // 2)
+        flops += 3 * (g * kp - 1) + 40
+        slots += 2 * (g * kp - 1) + 25
+        s += g
+    return flops, slots
 
 
 class ClockSampler:
@@ -191,7 +199,7 @@ def run_ours(args, link, ws, rank, local):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(device=dev)
-    eng = isrs.Engine(link, device=local)
+    eng = isrs.Engine(link, device=local, precision=args.precision)
     n = link.n_ch
     eta = torch.empty(n, dtype=torch.float64, device=dev)
     terms = torch.empty((n, 5), dtype=torch.float64, device=dev)
@@ -242,9 +250,12 @@ def run_ours(args, link, ws, rank, local):
     kc_ms = float(np.mean([k[0][1] for k in kern_ms]))
     kr_ms = float(np.mean([k[0][2] for k in kern_ms]))
     ps_d = kern_ms[-1][1][0]
-    fpp = algorithmic_flops_per_point(link) / link.n_span      # flops per point-span (mean)
+    chain_g, k_s = eng.span_chains()
+    fpp, spp = (v / link.n_span for v in algorithmic_work_per_point(chain_g, k_s))  # per point-span
     ach = ps_d * fpp / (kd_ms * 1e-3) / 1e12
     peak = fp64_peak_tflops()
+    slots_ach = ps_d * spp / (kd_ms * 1e-3) / 1e12
+    slots_peak = SMS * FP64_LANES * SM_MAX_MHZ * 1e6 / 1e12
 
     # end to end through the public API with host buffers: create + nli + D2H + destroy
     e2e = None
@@ -254,7 +265,7 @@ def run_ours(args, link, ws, rank, local):
         t_e2e = []
         for k in range(max(1, min(3, args.steps))):
             t0 = time.perf_counter()
-            isrs.eta_host(link, device=local)
+            isrs.eta_host(link, device=local, precision=args.precision)
             t_e2e.append(time.perf_counter() - t0)
         e2e = {"value": ws * pspans / float(np.median(t_e2e)), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 8 * n,
@@ -264,7 +275,8 @@ def run_ours(args, link, ws, rank, local):
         value = ws * pspans / (ms_max * 1e-3)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64" if args.precision == 64 else "f32 (mixed, row a8)", "data": "synthetic",
                 "config": config_desc(link, args),
                 "channels_per_s": ws * n / (ms_max * 1e-3),
                 "point_spans_per_step": pspans, "points_per_step": pts, "regions_per_step": nreg,
@@ -273,7 +285,13 @@ def run_ours(args, link, ws, rank, local):
                              "frac": ach / peak, "traffic": None,
                              "kernel": "isrs::integrand_kernel<false,0> (D-only regions)",
                              "flops_per_point_span": fpp,
-                             "peak_note": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz"},
+                             "span_chains": [int(g) for g in chain_g],
+                             "peak_note": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz "
+                                          "(DFMA microbenchmark on this pool: 34.1 TFLOP/s)"},
+                "fp64_pipe_slots": {"achieved": slots_ach, "peak": slots_peak, "unit": "T slot/s",
+                                    "frac": slots_ach / slots_peak, "per_point_span": spp,
+                                    "note": "same algorithmic count with DFMA and DADD one FP64 "
+                                            "pipe issue slot each (the recurrence's real bound)"},
                 "pct_fp64_peak": 100.0 * ach / peak,
                 "gpu_launches": launches_per_step * args.steps,
                 "clocks": clk, "e2e": e2e,
@@ -293,6 +311,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", type=int, default=64, choices=[64, 32],
+                    help="64: the fp64 hot path (default); 32: the mixed fp32 variant (row a8)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=8.0, help="CPU seconds per reference step")

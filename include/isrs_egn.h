@@ -120,6 +120,11 @@ ISRS_EGN_API int isrs_egn_eta_host(const isrs_egn_problem *p, const isrs_egn_num
  * launch processed ([0], [1]) and their sum ([2]). */
 ISRS_EGN_API int isrs_egn_last_kernel_ms(isrs_egn_t *h, double *ms_out, double *point_spans_out);
 
+/* Span chains of the handle (reading R9): *n_chain chains; chain_g (or NULL, capacity n_span)
+ * receives the number of spans G_c of each chain, k_s (or NULL, capacity n_span) the segment
+ * count K_s of every span.  Spans of a chain are consecutive; sum_c G_c = n_span. */
+ISRS_EGN_API int isrs_egn_span_chains(const isrs_egn_t *h, int32_t *n_chain, int32_t *chain_g, int32_t *k_s);
+
 /* Number of kernel launches the most recent isrs_egn_nli() enqueued (for bench accounting). */
 ISRS_EGN_API int isrs_egn_last_launch_count(const isrs_egn_t *h);
 

@@ -92,6 +92,15 @@ class Engine:
         _abi.check(_abi.get().isrs_egn_last_kernel_ms(self._h, ms, ps))
         return list(ms), list(ps)
 
+    def span_chains(self):
+        """(chain sizes G_c, K_s per span) of the handle's span chains (reading R9)."""
+        n = ctypes.c_int32()
+        g = np.zeros(self.n_span, dtype=np.int32)
+        k = np.zeros(self.n_span, dtype=np.int32)
+        _abi.check(_abi.get().isrs_egn_span_chains(self._h, ctypes.byref(n), g.ctypes.data_as(_abi._ip),
+                                                 k.ctypes.data_as(_abi._ip)))
+        return g[:n.value].copy(), k
+
     def last_launch_count(self):
         return _abi.get().isrs_egn_last_launch_count(self._h)
 

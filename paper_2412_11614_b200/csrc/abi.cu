@@ -81,6 +81,7 @@ struct isrs_egn {
   DevBuf<double> d_A2, d_A3, d_Eh, d_ah, d_gh, d_macc, d_aL;
   DevBuf<int> d_K, d_cls, d_Kc, d_chain_s0, d_chain_g;
   int n_chain = 0;
+  std::vector<int> chain_g, k_s;
   DevBuf<double> d_lnA, d_zeta;
   int kstride = 0, tstride = 0, tw = 0;
   // work list cache (last call)
@@ -117,7 +118,8 @@ static int validate(const isrs_egn_problem* p, const isrs_egn_numerics* n) {
   if (!is_fin(n->delta_z_m) || n->delta_z_m <= 0) return fail(ISRS_EGN_EINVAL, "delta_z_m <= 0");
   if (n->precision != 64 && n->precision != 32 && n->precision != 0)
     return fail(ISRS_EGN_EUNSUPPORTED, "precision must be 64 or 32");
-  if (n->precision == 32) return fail(ISRS_EGN_EUNSUPPORTED, "fp32 variant not built in this version");
+  if (n->precision == 32 && n->mu_mode != ISRS_EGN_MU_SEGMENT)
+    return fail(ISRS_EGN_EUNSUPPORTED, "precision 32 (row a8) is a variant of the segment mode only");
   if (n->mu_mode != ISRS_EGN_MU_SEGMENT && n->mu_mode != ISRS_EGN_MU_MACLAURIN)
     return fail(ISRS_EGN_EUNSUPPORTED, "unknown mu_mode");
   const double lim = 4.0e15;  // |values| < 2^52: integer-Hz arithmetic exact
@@ -244,7 +246,7 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
   // gamma, C_r, hence the same z = e^{i chi h} and envelope table) with an even K_s share one
   // recurrence over G * K_s segments, G * K_s <= CHAIN_MAX.  Segment mode only.
   std::vector<int> ch_s0, ch_g;
-  const bool chain_ok = num.mu_mode == ISRS_EGN_MU_SEGMENT &&
+  const bool chain_ok = num.mu_mode == ISRS_EGN_MU_SEGMENT && num.precision == 64 &&
                         !(num.flags & (ISRS_EGN_FLAG_NO_CHAIN | ISRS_EGN_FLAG_UNIT_LINK));
   for (int s = 0; s < p->n_span; ++s) {
     const bool same = s > 0 && chain_ok && (K[s] % 2 == 0) && p->length_m[s] == p->length_m[s - 1] &&
@@ -262,6 +264,8 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
     }
   }
   h->n_chain = (int)ch_s0.size();
+  h->chain_g = ch_g;
+  h->k_s = K;
   int kmax = *std::max_element(cK.begin(), cK.end());
   int kpad = (kmax + 1) & ~1;
   h->kstride = kpad;
@@ -305,13 +309,60 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
   return ISRS_EGN_OK;
 }
 
-// Region enumeration for the given COIs (canonical order: COI, then k1, then k2).
+// Number of in-support grid points of region (f, k1, k2), counted per lattice line j = a m1 + b m2
+// (f3 constant on a line) -- the integrand kernel's cost of the region.  Used only to order the
+// launch list (largest regions first, so the last wave of CTAs is short); ties at touching band
+// edges may be counted twice, which does not matter for ordering.
+static long long region_points(const isrs_egn* h, double f, int k1, int k2) {
+  const int N = h->N, nc = h->n_ch;
+  const long long r1 = h->rate[k1], r2 = h->rate[k2];
+  long long x = r1, y = r2;
+  while (y) { const long long t = x % y; x = y; y = t; }
+  const int a = (int)(r1 / x), b = (int)(r2 / x);
+  const double d1 = h->delta[k1], d2 = h->delta[k2];
+  const double g = d1 / a;
+  const double C = h->lo[k1] + h->lo[k2] - f + (0.5 * d1 + 0.5 * d2);
+  const int J = (a + b) * (N - 1) + 1;
+  long long cnt = 0;
+  if (a == 1 && b == 1) {
+    auto P = [&](long long j) -> long long {   // sum_{i<=j} min(i, 2N-2-i) + 1
+      if (j < 0) return 0;
+      if (j < N) return (j + 1) * (j + 2) / 2;
+      return (long long)N * N - (2LL * N - 2 - j) * (2LL * N - 1 - j) / 2;
+    };
+    const double f3max = C + g * (J - 1);
+    for (int c = (int)(std::lower_bound(h->hi.begin(), h->hi.end(), C) - h->hi.begin());
+         c < nc && h->lo[c] <= f3max; ++c) {
+      const long long j0 = std::max(0LL, (long long)std::ceil((h->lo[c] - C) / g));
+      const long long j1 = std::min((long long)J - 1, (long long)std::floor((h->hi[c] - C) / g));
+      if (j0 <= j1) cnt += P(j1) - P(j0 - 1);
+    }
+    return cnt;
+  }
+  int c = (int)(std::lower_bound(h->hi.begin(), h->hi.end(), C) - h->hi.begin());
+  for (int j = 0; j < J; ++j) {
+    const double f3 = C + g * j;
+    while (c < nc && h->hi[c] < f3) ++c;
+    if (c >= nc) break;
+    if (h->lo[c] > f3) continue;
+    int lowb = j - b * (N - 1);
+    lowb = (lowb <= 0) ? 0 : (lowb + a - 1) / a;
+    const int upb = std::min(N - 1, j / a);
+    for (int m1 = lowb; m1 <= upb; ++m1)
+      if ((j - a * m1) % b == 0) ++cnt;
+  }
+  return cnt;
+}
+
+// Region enumeration for the given COIs (canonical order: COI, then k1, then k2).  The launch
+// lists are ordered by decreasing region cost (stable), the partials stay indexed canonically.
 static void build_worklist(const isrs_egn* h, const std::vector<int>& coi, WorkList* w) {
   w->coi = coi;
   w->desc.clear();
   w->coi_off.assign(1, 0);
   w->list_d.clear();
   w->list_c.clear();
+  std::vector<long long> cost;
   const int nc = h->n_ch;
   for (int kappa : coi) {
     const double f = h->f[kappa];
@@ -334,10 +385,14 @@ static void build_worklist(const isrs_egn* h, const std::vector<int>& coi, WorkL
         const int id = (int)w->desc.size();
         w->desc.push_back(RegionDesc{kappa, k1, k2, flags});
         (flags ? w->list_c : w->list_d).push_back(id);
+        cost.push_back(region_points(h, f, k1, k2));
       }
     }
     w->coi_off.push_back((long long)w->desc.size());
   }
+  auto by_cost = [&](int x, int y) { return cost[x] > cost[y]; };
+  std::stable_sort(w->list_d.begin(), w->list_d.end(), by_cost);
+  std::stable_sort(w->list_c.begin(), w->list_c.end(), by_cost);
 }
 
 extern "C" int isrs_egn_nli(isrs_egn_t* h, int32_t n_coi, const int32_t* coi, double* eta_dev,
@@ -383,7 +438,8 @@ extern "C" int isrs_egn_nli(isrs_egn_t* h, int32_t n_coi, const int32_t* coi, do
   kp.kstride = h->kstride; kp.tstride = h->tstride; kp.tw = h->tw; kp.N = h->N;
   kp.desc = h->d_desc.p; kp.partials = h->d_partials.p;
   kp.mode = (h->num.flags & ISRS_EGN_FLAG_UNIT_LINK) ? MODE_UNIT
-            : (h->num.mu_mode == ISRS_EGN_MU_MACLAURIN ? MODE_MACLAURIN : MODE_SEGMENT);
+            : (h->num.mu_mode == ISRS_EGN_MU_MACLAURIN ? MODE_MACLAURIN
+               : (h->num.precision == 32 ? MODE_SEG32 : MODE_SEGMENT));
   if (!h->ev[0]) {
     for (auto& e : h->ev)
       if (cudaEventCreate(&e) != cudaSuccess) return cuda_fail(cudaGetLastError(), "cudaEventCreate");
@@ -474,6 +530,16 @@ extern "C" int isrs_egn_last_kernel_ms(isrs_egn_t* h, double* ms_out, double* po
     point_spans_out[1] = b * h->n_span;
     point_spans_out[2] = (a + b) * h->n_span;
   }
+  return ISRS_EGN_OK;
+}
+
+extern "C" int isrs_egn_span_chains(const isrs_egn_t* h, int32_t* n_chain, int32_t* chain_g, int32_t* k_s) {
+  if (!h || !n_chain) return fail(ISRS_EGN_EINVAL, "bad argument");
+  *n_chain = h->n_chain;
+  if (chain_g)
+    for (int c = 0; c < h->n_chain; ++c) chain_g[c] = h->chain_g[c];
+  if (k_s)
+    for (int s = 0; s < h->n_span; ++s) k_s[s] = h->k_s[s];
   return ISRS_EGN_OK;
 }
 

@@ -29,17 +29,19 @@ constexpr int TW_MAX = ISRS_TW;     // envelope-table rows (f3-lines) resident i
 constexpr int T_BYTES = ISRS_TBYTES;  // smem budget of the envelope table
 constexpr int LPT = LINE_CAP / BLOCK;  // lattice lines scanned per thread
 #ifndef ISRS_CHAIN_MAX
-#define ISRS_CHAIN_MAX 400
+#define ISRS_CHAIN_MAX 800
 #endif
 // longest chained recurrence (segments): the phase of the implicit z^n drifts by <= n^2 eps
-// (fl(2 cos(chi h)) is exact to eps), 400^2 * 1.1e-16 = 1.8e-11 relative per point (DESIGN R9)
+// (fl(2 cos(chi h)) is exact to eps), 800^2 * 1.1e-16 = 7e-11 relative per point (DESIGN R9)
 constexpr int CHAIN_MAX = ISRS_CHAIN_MAX;
 static_assert(LINE_CAP % BLOCK == 0, "LINE_CAP must be a multiple of BLOCK");
 
 // region flags (reading C8: a term whose gate or weight is zero is not evaluated)
 enum : int { NEED_E = 1, NEED_F = 2, NEED_G = 4, NEED_H = 8 };
 
-enum : int { MODE_SEGMENT = 0, MODE_MACLAURIN = 1, MODE_UNIT = 2 };
+// MODE_SEG32: row a8, the mixed fp32 variant of the segment form (fp32 recurrence, mu, phase
+// factor; fp64 chi h and its exact reduction, the phase advance and every accumulation)
+enum : int { MODE_SEGMENT = 0, MODE_MACLAURIN = 1, MODE_UNIT = 2, MODE_SEG32 = 3 };
 
 struct RegionDesc {
   int kappa, k1, k2, flags;

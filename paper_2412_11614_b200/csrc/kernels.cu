@@ -29,6 +29,12 @@
 
 #include "internal.h"
 
+#ifndef ISRS_UNROLL
+#define ISRS_UNROLL 4
+#endif
+#define ISRS_STR(x) #x
+#define ISRS_UNROLL_PRAGMA(n) _Pragma(ISRS_STR(unroll n))
+
 namespace isrs {
 
 // ------------------------------------------------------------------------------------------
@@ -177,9 +183,9 @@ __device__ inline double block_sum(double v, double* red) {
   return r;
 }
 
-// index i with sl_start[i] <= p < sl_start[i+1]
-__device__ inline int line_of(const int* sl_start, int S, int p) {
-  int lo = 0, hi = S - 1;
+// index i with sl_start[i] <= p < sl_start[i+1], searched in [lo, S-1]
+__device__ inline int line_of(const int* sl_start, int S, int p, int lo = 0) {
+  int hi = S - 1;
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
     if (sl_start[mid] <= p) lo = mid; else hi = mid - 1;
@@ -386,7 +392,18 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
       // groups), so one envelope-table row serves all PPT recurrences of the thread
       const int slot0 = p0 + PPT * tid;
       const bool gvalid = slot0 < p_end;
-      const int li = gvalid ? line_of(sm.sl_start, S, slot0) : i_first;
+      // line of this thread's group: one (warp-uniform, broadcast) search for the line i0 of
+      // the warp's first group, then the <= 31 later line starts inside the warp's 32 groups
+      // are OR-ed into a position mask (lines are padded to whole groups, so each starts on
+      // its own group): line = i0 + #starts at positions <= lane
+      const int lane = tid & 31;
+      const int wslot0 = p0 + PPT * (tid & ~31);
+      const bool wact = wslot0 < p_end;                    // warp has at least one valid group
+      const int i0 = wact ? line_of(sm.sl_start, S, wslot0, i_first) : i_first;
+      int pos = 32;
+      if (lane < 31 && i0 + 1 + lane < S) pos = (sm.sl_start[i0 + 1 + lane] - wslot0) / PPT;
+      const unsigned starts = __reduce_or_sync(0xffffffffu, (pos < 32) ? (1u << pos) : 0u);
+      const int li = gvalid ? i0 + __popc(starts & ((2u << lane) - 1u)) : i_first;
       const int lj = sm.sl_j[li];
       const int kq0 = slot0 - sm.sl_start[li];
       const int lcnt = sm.sl_cnt[li];
@@ -418,7 +435,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
           // chain of G identical consecutive spans starting at s (G = 1 unless chained, R9)
           const int s = __ldg(p.chain_s0 + ch), G = __ldg(p.chain_g + ch);
           const int cls = __ldg(p.cls + s);
-          if (MODE == MODE_SEGMENT &&
+          if ((MODE == MODE_SEGMENT || MODE == MODE_SEG32) &&
               (cls != tcls || i_first < tb || i_last >= tb + tn)) {
             // ---- (re)build the envelope table rows for compacted lines [tb, tb + tn)
             __syncthreads();
@@ -426,22 +443,110 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
             tn = (p.n_cls == 1) ? min(p.tw, S - i_first) : (i_last - i_first + 1);
             tcls = cls;
             const int Kc = __ldg(p.Kc + cls);
-            const int Kp = (Kc + 1) & ~1;
+            // fp64 rows: K rounded up to even (16-byte pair loads); fp32 rows (a8): to a
+            // multiple of 4 (float4 loads), row stride 2 tstride floats
+            const int Kp = (MODE == MODE_SEG32) ? ((Kc + 3) & ~3) : ((Kc + 1) & ~1);
+            float* T32 = reinterpret_cast<float*>(sm.T);
             const double* lnA = p.lnA + (size_t)cls * p.kstride;
             const double* zt = p.zeta + (size_t)cls * p.kstride;
-            for (int e = tid; e < tn * Kp; e += BLOCK) {
-              const int row = e / Kp, ii = e - row * Kp;
+            // one thread per coefficient k walks the rows: a'_k(f3 + g) = a'_k(f3) e^{-zeta_k g}
+            // (one DMUL per entry; rows whose line index jumps restart from exp; <= tw steps,
+            // relative error <= tw eps)
+            for (int ii = tid; ii < Kp; ii += BLOCK) {
               const int k = Kp - 1 - ii;
-              const double f3 = __dadd_rn(C, g * (double)sm.sl_j[tb + row]);
-              const double v = (k < Kc) ? exp(__ldg(lnA + k) - __ldg(zt + k) * f3) : 0.0;
-              sm.T[row * p.tstride + ii] = v;
-              if (ii < 2) sm.T[row * p.tstride + Kp + ii] = v;   // wrap pair for span chains (R9)
+              const bool live = k < Kc;
+              const double la = live ? __ldg(lnA + k) : 0.0, ze = live ? __ldg(zt + k) : 0.0;
+              const double step = exp(-ze * g);
+              double v = 0.0;
+              int jprev = -2;
+              for (int row = 0; row < tn; ++row) {
+                const int j = sm.sl_j[tb + row];
+                if (live) v = (j == jprev + 1) ? v * step : exp(la - ze * __dadd_rn(C, g * (double)j));
+                jprev = j;
+                if (MODE == MODE_SEG32) {
+                  T32[row * 2 * p.tstride + ii] = (float)v;
+                } else {
+                  sm.T[row * p.tstride + ii] = v;
+                  if (ii < 2) sm.T[row * p.tstride + Kp + ii] = v;   // wrap pair for span chains (R9)
+                }
+              }
             }
             __syncthreads();
           }
+          if (!wact) continue;   // warp-uniform: idle warps of a ragged last chunk skip the math
           const double A2 = __ldg(p.A2 + s), A3 = __ldg(p.A3 + s);
           const double Eh = __ldg(p.Eh + s), ah = __ldg(p.ah + s), gh = __ldg(p.gh + s);
           const int Ks = __ldg(p.K + s);
+          if (MODE == MODE_SEG32) {
+            // ---- row a8: mixed fp32 variant (no span chains).  chi h / pi and its reduction
+            // mod 2 stay fp64 (exact); z = cis(pi r) by sincospif; the recurrence runs on pairs
+            // of points with packed FFMA2; I_0, mu and the span phase factor in fp32; the phase
+            // advance and Y accumulate in fp64.
+            const float Ehf = (float)Eh, ahf = (float)ah, ghf = (float)gh;
+            const int Kp4 = (__ldg(p.Kc + cls) + 3) & ~3;
+            const float4* rowq =
+                reinterpret_cast<const float4*>(reinterpret_cast<const float*>(sm.T) + (li - tb) * 2 * p.tstride);
+            double xs[PPT];
+            float sf[PPT], cf[PPT];
+            float2 c2[PPT / 2], b1[PPT / 2], b2[PPT / 2];
+#pragma unroll
+            for (int q = 0; q < PPT; ++q) {
+              xs[q] = uv[q] * fma(A3, Ssum[q], A2);                 // chi h / pi
+              const double r = xs[q] - 2.0 * rint(0.5 * xs[q]);     // exact, |r| <= 1
+              sincospif((float)r, &sf[q], &cf[q]);
+            }
+#pragma unroll
+            for (int hq = 0; hq < PPT / 2; ++hq) {
+              c2[hq] = make_float2(2.f * cf[2 * hq], 2.f * cf[2 * hq + 1]);
+              b1[hq] = make_float2(0.f, 0.f);
+              b2[hq] = make_float2(0.f, 0.f);
+            }
+            const float2 neg1 = make_float2(-1.f, -1.f);
+            auto step = [&](float a) {
+#pragma unroll
+              for (int hq = 0; hq < PPT / 2; ++hq) {
+                const float2 t = __ffma2_rn(b2[hq], neg1, make_float2(a, a));   // a - b_{k+2}
+                const float2 n = __ffma2_rn(c2[hq], b1[hq], t);
+                b2[hq] = b1[hq];
+                b1[hq] = n;
+              }
+            };
+            const int n4 = Kp4 >> 2;
+            float4 tc = rowq[0];
+#pragma unroll 2
+            for (int i4 = 0; i4 < n4 - 1; ++i4) {
+              const float4 tn = rowq[i4 + 1];
+              step(tc.x);
+              step(tc.y);
+              step(tc.z);
+              step(tc.w);
+              tc = tn;
+            }
+            step(tc.x);
+            step(tc.y);
+            step(tc.z);                                             // -> b_1, b_2
+#pragma unroll
+            for (int q = 0; q < PPT; ++q) {
+              const float bb1 = (q & 1) ? b1[q >> 1].y : b1[q >> 1].x;
+              const float bb2 = (q & 1) ? b2[q >> 1].y : b2[q >> 1].x;
+              const float accr = fmaf(cf[q], bb1, tc.w - bb2);       // a'_0 + z b_1 - b_2
+              const float acci = sf[q] * bb1;
+              const float px = (float)(CUDART_PI * xs[q]);
+              const float wr1 = fmaf(Ehf, cf[q], -1.f), wi = Ehf * sf[q];
+              const float inv = __fdividef(ghf, fmaf(px, px, ahf * ahf));
+              const float nr = fmaf(wi, px, -ahf * wr1);
+              const float ni = -fmaf(px, wr1, ahf * wi);
+              const float mr = (nr * accr - ni * acci) * inv;
+              const float mi = (nr * acci + ni * accr) * inv;
+              float ps = 0.f, pc = 1.f;
+              if (ch > 0) __sincosf(CUDART_PI_F * (float)th[q], &ps, &pc);
+              yr[q] += (double)fmaf(mr, pc, -mi * ps);
+              yi[q] += (double)fmaf(mr, ps, mi * pc);
+              const double t2 = fma(xs[q], (double)Ks, th[q]);
+              th[q] = t2 - 2.0 * rint(0.5 * t2);
+            }
+            continue;
+          }
           double x[PPT], sn[PPT], cs[PPT];
 #pragma unroll
           for (int q = 0; q < PPT; ++q) {
@@ -468,7 +573,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
             double2 tc = rowp[0];
             for (int gi = 0; gi < G; ++gi) {
               const int nit = (gi == G - 1) ? npair - 1 : npair;
-#pragma unroll 4
+              ISRS_UNROLL_PRAGMA(ISRS_UNROLL)
               for (int i2 = 0; i2 < nit; ++i2) {
                 const double2 tn = rowp[i2 + 1];
                 double n0[PPT];
@@ -527,8 +632,8 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
               mi = (eta_i - cf * (eta_i - et2_i)) * gh;
             }
             // Y += gamma_s mu_s e^{i theta_s}, theta_s = pi * th (reading C3)
-            double ps, pc;
-            sincospi_d(th[q], &ps, &pc);
+            double ps = 0.0, pc = 1.0;                  // theta_1 = 0 for the first chain
+            if (ch > 0) sincospi_d(th[q], &ps, &pc);
             yr[q] = fma(mr, pc, fma(-mi, ps, yr[q]));
             yi[q] = fma(mr, ps, fma(mi, pc, yi[q]));
             double t2 = fma(x[q], (double)(Ks * G), th[q]);   // theta += chi_s L_s (x G spans)
@@ -656,10 +761,12 @@ int launch_integrand(const KParams& p, const int* list, long long n_list, bool c
   *n_launches += 1;
   if (coherent) {
     if (p.mode == MODE_SEGMENT) return launch_one<true, MODE_SEGMENT>(p, list, n_list, st);
+    if (p.mode == MODE_SEG32) return launch_one<true, MODE_SEG32>(p, list, n_list, st);
     if (p.mode == MODE_MACLAURIN) return launch_one<true, MODE_MACLAURIN>(p, list, n_list, st);
     return launch_one<true, MODE_UNIT>(p, list, n_list, st);
   }
   if (p.mode == MODE_SEGMENT) return launch_one<false, MODE_SEGMENT>(p, list, n_list, st);
+  if (p.mode == MODE_SEG32) return launch_one<false, MODE_SEG32>(p, list, n_list, st);
   if (p.mode == MODE_MACLAURIN) return launch_one<false, MODE_MACLAURIN>(p, list, n_list, st);
   return launch_one<false, MODE_UNIT>(p, list, n_list, st);
 }

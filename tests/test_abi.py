@@ -28,7 +28,7 @@ def test_header_declares_the_boundary():
     syms = declared_symbols()
     for s in ("isrs_egn_create", "isrs_egn_nli", "isrs_egn_destroy"):
         assert s in syms
-    assert len(syms) == 10
+    assert len(syms) == 11
 
 
 def test_library_exports_every_declared_symbol(abi):
@@ -68,6 +68,8 @@ def test_validation_errors_before_any_cuda(abi):
     assert rc == abi.EINVAL and "delta_z" in msg
     rc, msg, _ = _create(abi, l, precision=16)
     assert rc == abi.EUNSUPPORTED
+    rc, msg, _ = _create(abi, l, precision=32, mu_mode=abi.MU_MACLAURIN)
+    assert rc == abi.EUNSUPPORTED and "segment" in msg
     bad = l.with_(f_center_hz=l.f_center_hz + 0.25)
     rc, msg, _ = _create(abi, bad)
     assert rc == abi.EINVAL and "integer" in msg

@@ -182,6 +182,34 @@ def test_span_chaining_matches_unchained(isrs, cfg, coi):
     assert np.all(np.abs(ta - tb) <= TOL_ETA * np.abs(tb).sum(axis=1, keepdims=True))
 
 
+DB_TOL_FP32 = 1e-3     # north star: optional fp32 path within 0.001 dB
+
+
+def _db(x):
+    return 10.0 * np.log10(x)
+
+
+@pytest.mark.parametrize("name", ["uniform_64gbd_2span", "three_islands_96gbd", "mixed_rates_guard",
+                                  "strong_isrs", "long_link_chained", "single_channel_N64"])
+def test_fp32_variant_vs_oracle_tiny(isrs, name):
+    """Row a8: the mixed fp32 variant stays within 0.001 dB of the fp64 oracle."""
+    link = tiny_link(**TINY[name])
+    e_o, _ = egn.eta(link)
+    e_g, _ = gpu_eta(isrs, link, precision=32)
+    assert np.all(np.abs(_db(e_g) - _db(e_o)) <= DB_TOL_FP32), (name, _db(e_g) - _db(e_o))
+
+
+@pytest.mark.parametrize("cfg,coi", [("c1", None), ("c2", None), ("c3", [0, 50, 99]), ("c4", [0, 40, 79]),
+                                     ("c5", [0, 100, 199])])
+def test_fp32_variant_vs_fp64_full_size(isrs, cfg, coi):
+    """Row a8 at BASELINE sizes: |eta_fp32 - eta_fp64| <= 0.001 dB for every requested COI."""
+    link = bj_config(cfg)
+    a, _ = gpu_eta(isrs, link, coi=coi, precision=32)
+    b, _ = gpu_eta(isrs, link, coi=coi)
+    d = np.abs(_db(a) - _db(b))
+    assert np.all(d <= DB_TOL_FP32), (cfg, d.max())
+
+
 def test_full_size_determinism_c2(isrs):
     link = bj_config("c2")
     with isrs.Engine(link) as e:

@@ -49,6 +49,24 @@ void run(const char* name, int threads, int sms, double* d, long long* dc) {
          mma_flops / c, fma_flops / c, (mma_flops + fma_flops) / c, c);
 }
 
+// dependent-chain latency: one warp per SM, a single chain of OP
+template <int OP>
+__global__ void lat(double* out, long long* cyc, int iters, double a, double b) {
+  double x = threadIdx.x * 1e-3;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      if (OP == 0) x = fma(x, a, b);
+      if (OP == 1) x = x + b;
+      if (OP == 2) x = x * a;
+    }
+  }
+  long long t1 = clock64();
+  if (x == 1.2345) out[0] = x;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 int main() {
   cudaDeviceProp p;
   cudaGetDeviceProperties(&p, 0);
@@ -61,6 +79,18 @@ int main() {
     run<0, 8>("DFMA", t, p.multiProcessorCount, d, dc);
     run<4, 8>("DMMA+DFMA", t, p.multiProcessorCount, d, dc);
     run<2, 16>("DMMA+2DFMA", t, p.multiProcessorCount, d, dc);
+  }
+  const char* nm[3] = {"DFMA", "DADD", "DMUL"};
+  for (int op = 0; op < 3; ++op) {
+    for (int rep = 0; rep < 2; ++rep) {
+      if (op == 0) lat<0><<<1, 32>>>(d, dc, 1000, 0.999999, 1e-9);
+      if (op == 1) lat<1><<<1, 32>>>(d, dc, 1000, 0.999999, 1e-9);
+      if (op == 2) lat<2><<<1, 32>>>(d, dc, 1000, 0.999999, 1e-9);
+    }
+    cudaDeviceSynchronize();
+    long long c = 0;
+    cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
+    printf("%s dependent-chain latency %.2f cycles\n", nm[op], c / 16000.0);
   }
   printf("%s (SM clock %d kHz)\n", cudaGetErrorString(cudaDeviceSynchronize()), p.clockRate);
 }
