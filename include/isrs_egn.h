@@ -78,6 +78,11 @@ typedef struct {
   int32_t precision;   /* 64 (fp64, default) | 32 (mixed fp32 variant, row a8)                  */
   int32_t mu_mode;     /* ISRS_EGN_MU_*                                                          */
   uint32_t flags;      /* ISRS_EGN_FLAG_*                                                        */
+  int32_t f_samples;   /* 0 (default): G_NLI at the COI centre, P_NLI = R G_NLI(f_kappa) (reading
+                          C1, the 2-D path).  n > 0: the 3-D form of Eqs. 17-21 (NEXT-3):
+                          f integrated over the COI band by the midpoint rule with n samples
+                          f_m = f_kappa - R/2 + (m + 1/2) R/n, P_NLI = sum_m G_NLI(f_m) R/n; requires
+                          every R_i / (2n) to be an integer (exact lattice, reading R3).  n x work. */
 } isrs_egn_numerics;
 
 /* Validate, canonicalise (f_c, B_tot, P_tot, K_s; reading C5), enumerate the regions of every

@@ -77,12 +77,25 @@ def grid(c: Canon, i: int) -> np.ndarray:
     return c.lo[i] + (np.arange(c.N) + 0.5) * c.delta[i]
 
 
-def region_points(c: Canon, kappa: int, k1: int, k2: int):
-    """Point arrays of region (kappa, k1, k2), indexed [m2, m1]."""
+def region_points(c: Canon, kappa: int, k1: int, k2: int, f=None):
+    """Point arrays of region (kappa, k1, k2), indexed [m2, m1]; f = the NLI frequency (the COI
+    centre c.f[kappa] unless given: 3-D mode, NEXT-3)."""
+    f = c.f[kappa] if f is None else f
     F1 = grid(c, k1)[None, :] * np.ones((c.N, 1))
     F2 = grid(c, k2)[:, None] * np.ones((1, c.N))
-    f3 = F1 + F2 - c.f[kappa]
+    f3 = F1 + F2 - f
     return F1, F2, f3
+
+
+def coi_frequencies(c: Canon, kappa: int, f_samples: int = 0):
+    """Frequencies f at which G_NLI is evaluated for COI kappa.
+    f_samples = 0: the COI centre only (reading C1, locally white: P_NLI = R_kappa G_NLI(f_kappa)).
+    f_samples = n > 0 (NEXT-3, the 3-D form): Eqs. 17-21 integrate f over the COI band
+    [-R/2, R/2] about kappa R; midpoint rule f_m = lo_kappa + (m + 1/2) R_kappa / n,
+    m = 0..n-1, so P_NLI = sum_m G_NLI(f_m) R_kappa / n."""
+    if f_samples <= 0:
+        return np.array([c.f[kappa]])
+    return c.lo[kappa] + (np.arange(f_samples) + 0.5) * (c.R[kappa] / f_samples)
 
 
 def island_gates(c: Canon, f3: np.ndarray):
@@ -99,9 +112,11 @@ def island_gates(c: Canon, f3: np.ndarray):
 
 
 def region_islands(c: Canon, kappa: int, k1: int, k2: int, mu_mode: str = "closed",
-                   need=("D", "E", "F", "G", "H")):
-    """Per-island raw integrals D, E, F, G, H of region (kappa, k1, k2) (Eqs. 17-21, C6, C7, C10)."""
-    F1, F2, f3 = region_points(c, kappa, k1, k2)
+                   need=("D", "E", "F", "G", "H"), f=None):
+    """Per-island raw integrals D, E, F, G, H of region (kappa, k1, k2) (Eqs. 17-21, C6, C7, C10)
+    at NLI frequency f (default: the COI centre)."""
+    f = c.f[kappa] if f is None else f
+    F1, F2, f3 = region_points(c, kappa, k1, k2, f)
     gates = island_gates(c, f3)
     if not gates:
         return []
@@ -112,7 +127,7 @@ def region_islands(c: Canon, kappa: int, k1: int, k2: int, mu_mode: str = "close
     if mu_mode == "unit":                           # test hook P6: Y := 1
         Y[support] = 1.0
     else:
-        Y[support] = link_mod.link_function(F1[support], F2[support], c.f[kappa], c.spans,
+        Y[support] = link_mod.link_function(F1[support], F2[support], f, c.spans,
                                             c.p_tot, c.b_tot, c.dz, mu_mode)
     d1, d2 = c.delta[k1], c.delta[k2]
     N = c.N
@@ -150,11 +165,12 @@ def region_islands(c: Canon, kappa: int, k1: int, k2: int, mu_mode: str = "close
     return res
 
 
-def has_support_bound(c: Canon, kappa: int, k1: int, k2: int) -> bool:
+def has_support_bound(c: Canon, kappa: int, k1: int, k2: int, f=None) -> bool:
     """Cheap necessary condition for a non-empty region: the f3 range of the bin centres
     overlaps some band."""
-    lo3 = c.lo[k1] + c.lo[k2] - c.f[kappa] + (c.delta[k1] + c.delta[k2]) / 2
-    hi3 = c.hi[k1] + c.hi[k2] - c.f[kappa] - (c.delta[k1] + c.delta[k2]) / 2
+    f = c.f[kappa] if f is None else f
+    lo3 = c.lo[k1] + c.lo[k2] - f + (c.delta[k1] + c.delta[k2]) / 2
+    hi3 = c.hi[k1] + c.hi[k2] - f - (c.delta[k1] + c.delta[k2]) / 2
     return bool(np.any((c.hi >= lo3) & (c.lo <= hi3)))
 
 
@@ -183,11 +199,12 @@ def island_contributions(c: Canon, k1: int, k2: int, isl: dict):
     return np.array([tD, tE, tF, tG, tH])
 
 
-def eta(link, coi=None, mu_mode: str = "closed", return_regions: bool = False):
+def eta(link, coi=None, mu_mode: str = "closed", return_regions: bool = False, f_samples: int = 0):
     """eta_kappa (1/W^2, Eq. 11 with P = P_kappa, reading C13) and the D/E/F/G/H breakdown.
 
     Brute force over every (kappa1, kappa2) pair and every grid point (Eq. 16 generalised to
-    arbitrary channel plans: an island exists wherever f3 lands in a band).
+    arbitrary channel plans: an island exists wherever f3 lands in a band).  f_samples > 0: the
+    3-D form (NEXT-3), G_NLI averaged over f_samples midpoints of the COI band (coi_frequencies).
     """
     c = canonicalize(link)
     n = c.f.size
@@ -197,18 +214,21 @@ def eta(link, coi=None, mu_mode: str = "closed", return_regions: bool = False):
     regions = {}
     for ci, kappa in enumerate(coi):
         acc = np.zeros(5)
-        for k1 in range(n):
-            for k2 in range(n):
-                if not has_support_bound(c, kappa, k1, k2):
-                    continue
-                isls = region_islands(c, kappa, k1, k2, mu_mode, _needed_terms(c, k1, k2))
-                if not isls:
-                    continue
-                if return_regions:
-                    regions[(kappa, k1, k2)] = isls
-                for isl in isls:
-                    acc = acc + island_contributions(c, k1, k2, isl)
-        scale = c.R[kappa] / c.P[kappa] ** 3           # P_NLI = R G_NLI (C1); Eq. 11
+        fs = coi_frequencies(c, kappa, f_samples)
+        for f in fs:
+            for k1 in range(n):
+                for k2 in range(n):
+                    if not has_support_bound(c, kappa, k1, k2, f):
+                        continue
+                    isls = region_islands(c, kappa, k1, k2, mu_mode, _needed_terms(c, k1, k2), f)
+                    if not isls:
+                        continue
+                    if return_regions:
+                        regions[(kappa, k1, k2) if f_samples <= 0 else (kappa, float(f), k1, k2)] = isls
+                    for isl in isls:
+                        acc = acc + island_contributions(c, k1, k2, isl)
+        # P_NLI = R G_NLI(f_kappa) (C1) or sum_m G_NLI(f_m) R / n (3-D); Eq. 11
+        scale = c.R[kappa] / c.P[kappa] ** 3 / len(fs)
         terms[ci] = acc * scale
         etas[ci] = acc.sum() * scale
     if return_regions:
@@ -271,6 +291,13 @@ def eta_db(eta_val):
     return 10.0 * np.log10(eta_val)
 
 
+def unit_link_eta_3d(phi, psi):
+    """Continuous limit of the 3-D unit-link pin (P14): single channel, Y := 1, f
+    averaged over the band: D = 2/3 R^2, E = F = G = R^3/2, H = 9/20 R^4
+    ->  eta = 32/81 + 48/81 Phi + 4/45 Psi."""
+    return 32.0 / 81.0 + 48.0 / 81.0 * phi + 4.0 / 45.0 * psi
+
+
 def unit_link_eta(phi, psi):
     """Closed form of pin P6: single channel, Y := 1, f at the centre:
     D = 3/4 R^2, E = F = G = 7/12 R^3, H = 9/16 R^4  ->  eta = 4/9 + 56/81 Phi + Psi/9 (1/W^2 units
@@ -280,4 +307,5 @@ def unit_link_eta(phi, psi):
 
 __all__ = ["Canon", "canonicalize", "grid", "region_points", "island_gates", "region_islands",
            "island_contributions", "eta", "region_partials", "eta_db", "unit_link_eta",
+           "unit_link_eta_3d", "coi_frequencies",
            "has_support_bound", "math"]

@@ -33,11 +33,11 @@ class Engine:
     """Handle over one link (isrs_egn_create / isrs_egn_nli / isrs_egn_destroy)."""
 
     def __init__(self, link, grid_n=None, delta_z_m=None, device=0, precision=64,
-                 mu_mode=MU_SEGMENT, flags=0):
+                 mu_mode=MU_SEGMENT, flags=0, f_samples=0):
         self._pa = ProblemArrays(link)
         n = numerics(grid_n if grid_n is not None else link.grid_n,
                      delta_z_m if delta_z_m is not None else getattr(link, "delta_z_m", 1000.0),
-                     precision, mu_mode, flags)
+                     precision, mu_mode, flags, f_samples)
         self.n_ch = self._pa.struct.n_ch
         self.n_span = self._pa.struct.n_span
         self.device = device
@@ -123,12 +123,12 @@ class Engine:
 
 
 def eta_host(link, coi=None, grid_n=None, delta_z_m=None, device=0, precision=64, mu_mode=MU_SEGMENT,
-             flags=0, terms=False):
+             flags=0, terms=False, f_samples=0):
     """One-shot end-to-end call with host buffers (isrs_egn_eta_host)."""
     pa = ProblemArrays(link)
     n = numerics(grid_n if grid_n is not None else link.grid_n,
                  delta_z_m if delta_z_m is not None else getattr(link, "delta_z_m", 1000.0),
-                 precision, mu_mode, flags)
+                 precision, mu_mode, flags, f_samples)
     if coi is None:
         nco, cp = pa.struct.n_ch, None
     else:

@@ -39,7 +39,7 @@ class Problem(ctypes.Structure):
 class Numerics(ctypes.Structure):
     _fields_ = [("grid_n", ctypes.c_int32), ("delta_z_m", ctypes.c_double),
                 ("precision", ctypes.c_int32), ("mu_mode", ctypes.c_int32),
-                ("flags", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("f_samples", ctypes.c_int32)]
 
 
 class IsrsEgnError(RuntimeError):
@@ -133,6 +133,6 @@ class ProblemArrays:
         return sum(a.nbytes for a in self._keep.values())
 
 
-def numerics(grid_n, delta_z_m=1000.0, precision=64, mu_mode=MU_SEGMENT, flags=0):
+def numerics(grid_n, delta_z_m=1000.0, precision=64, mu_mode=MU_SEGMENT, flags=0, f_samples=0):
     return Numerics(grid_n=int(grid_n), delta_z_m=float(delta_z_m), precision=int(precision),
-                    mu_mode=int(mu_mode), flags=int(flags))
+                    mu_mode=int(mu_mode), flags=int(flags), f_samples=int(f_samples))

@@ -60,6 +60,7 @@ struct DevBuf {
 
 struct WorkList {
   std::vector<int> coi;
+  std::vector<double> fv;   // NLI frequency of each (COI, f sample)
   std::vector<RegionDesc> desc;
   std::vector<long long> coi_off;
   std::vector<int> list_d, list_c;
@@ -90,6 +91,7 @@ struct isrs_egn {
   DevBuf<RegionDesc> d_desc;
   DevBuf<long long> d_coi_off;
   DevBuf<int> d_coi, d_list_d, d_list_c;
+  DevBuf<double> d_fv;
   DevBuf<double> d_partials, d_npts;
   cudaStream_t last_stream = nullptr;
   bool have_result = false;
@@ -120,6 +122,7 @@ static int validate(const isrs_egn_problem* p, const isrs_egn_numerics* n) {
     return fail(ISRS_EGN_EUNSUPPORTED, "precision must be 64 or 32");
   if (n->precision == 32 && n->mu_mode != ISRS_EGN_MU_SEGMENT)
     return fail(ISRS_EGN_EUNSUPPORTED, "precision 32 (row a8) is a variant of the segment mode only");
+  if (n->f_samples < 0 || n->f_samples > 4096) return fail(ISRS_EGN_EINVAL, "f_samples must be in [0, 4096]");
   if (n->mu_mode != ISRS_EGN_MU_SEGMENT && n->mu_mode != ISRS_EGN_MU_MACLAURIN)
     return fail(ISRS_EGN_EUNSUPPORTED, "unknown mu_mode");
   const double lim = 4.0e15;  // |values| < 2^52: integer-Hz arithmetic exact
@@ -133,6 +136,11 @@ static int validate(const isrs_egn_problem* p, const isrs_egn_numerics* n) {
     const double half = R / (2.0 * n->grid_n);
     if (half != std::floor(half))
       return fail(ISRS_EGN_EINVAL, "symbol_rate_hz" + at + " / (2 grid_n) must be an integer (C10)");
+    if (n->f_samples > 0) {
+      const double hf = R / (2.0 * n->f_samples);
+      if (hf != std::floor(hf))
+        return fail(ISRS_EGN_EINVAL, "symbol_rate_hz" + at + " / (2 f_samples) must be an integer (R3)");
+    }
     if (!is_fin(P) || P <= 0) return fail(ISRS_EGN_EINVAL, "launch_power_w" + at + " must be > 0");
     if (!is_fin(p->excess_kurtosis[i])) return fail(ISRS_EGN_EINVAL, "excess_kurtosis" + at);
     if (p->psi && !is_fin(p->psi[i])) return fail(ISRS_EGN_EINVAL, "psi" + at);
@@ -358,14 +366,21 @@ static long long region_points(const isrs_egn* h, double f, int k1, int k2) {
 // lists are ordered by decreasing region cost (stable), the partials stay indexed canonically.
 static void build_worklist(const isrs_egn* h, const std::vector<int>& coi, WorkList* w) {
   w->coi = coi;
+  w->fv.clear();
   w->desc.clear();
   w->coi_off.assign(1, 0);
   w->list_d.clear();
   w->list_c.clear();
   std::vector<long long> cost;
   const int nc = h->n_ch;
+  const int fs = h->num.f_samples, nfs = std::max(1, fs);
   for (int kappa : coi) {
-    const double f = h->f[kappa];
+   for (int m = 0; m < nfs; ++m) {
+    // NLI frequency: the COI centre (C1), or the 3-D midpoint sample f_m (exact: R/(2 fs) in Z)
+    const double f = (fs == 0) ? h->f[kappa]
+                               : h->lo[kappa] + (2.0 * m + 1.0) * (h->R[kappa] / (2.0 * fs));
+    const int fvi = (int)w->fv.size();
+    w->fv.push_back(f);
     for (int k1 = 0; k1 < nc; ++k1) {
       for (int k2 = 0; k2 < nc; ++k2) {
         const double lo3 = h->lo[k1] + h->lo[k2] - f + (h->delta[k1] + h->delta[k2]) / 2;
@@ -383,11 +398,12 @@ static void build_worklist(const isrs_egn* h, const std::vector<int>& coi, WorkL
           // unit link hook: same gating
         }
         const int id = (int)w->desc.size();
-        w->desc.push_back(RegionDesc{kappa, k1, k2, flags});
+        w->desc.push_back(RegionDesc{kappa, k1, k2, flags | (fvi << FV_SHIFT)});
         (flags ? w->list_c : w->list_d).push_back(id);
         cost.push_back(region_points(h, f, k1, k2));
       }
     }
+   }
     w->coi_off.push_back((long long)w->desc.size());
   }
   auto by_cost = [&](int x, int y) { return cost[x] > cost[y]; };
@@ -422,7 +438,8 @@ extern "C" int isrs_egn_nli(isrs_egn_t* h, int32_t n_coi, const int32_t* coi, do
     build_worklist(h, c, &h->wl);
     bool ok = h->d_desc.upload(h->wl.desc) && h->d_coi_off.upload(h->wl.coi_off) &&
               h->d_coi.upload(h->wl.coi) && h->d_list_d.upload(h->wl.list_d) &&
-              h->d_list_c.upload(h->wl.list_c) && h->d_partials.alloc(h->wl.desc.size() * 6) &&
+              h->d_list_c.upload(h->wl.list_c) && h->d_fv.upload(h->wl.fv) &&
+              h->d_partials.alloc(h->wl.desc.size() * 6) &&
               h->d_npts.alloc(c.size());
     if (!ok) return fail(ISRS_EGN_ENOMEM, "work-list allocation failed");
   }
@@ -436,7 +453,7 @@ extern "C" int isrs_egn_nli(isrs_egn_t* h, int32_t n_coi, const int32_t* coi, do
   kp.chain_s0 = h->d_chain_s0.p; kp.chain_g = h->d_chain_g.p; kp.n_chain = h->n_chain;
   kp.lnA = h->d_lnA.p; kp.zeta = h->d_zeta.p; kp.Kc = h->d_Kc.p; kp.n_cls = h->n_cls;
   kp.kstride = h->kstride; kp.tstride = h->tstride; kp.tw = h->tw; kp.N = h->N;
-  kp.desc = h->d_desc.p; kp.partials = h->d_partials.p;
+  kp.fv = h->d_fv.p; kp.desc = h->d_desc.p; kp.partials = h->d_partials.p;
   kp.mode = (h->num.flags & ISRS_EGN_FLAG_UNIT_LINK) ? MODE_UNIT
             : (h->num.mu_mode == ISRS_EGN_MU_MACLAURIN ? MODE_MACLAURIN
                : (h->num.precision == 32 ? MODE_SEG32 : MODE_SEGMENT));
@@ -455,7 +472,8 @@ extern "C" int isrs_egn_nli(isrs_egn_t* h, int32_t n_coi, const int32_t* coi, do
   h->launched[0] = !h->wl.list_d.empty();
   h->launched[1] = !h->wl.list_c.empty();
   RParams rp{h->d_desc.p, h->d_partials.p, h->d_coi_off.p, h->d_coi.p, h->d_G.p, h->d_R.p,
-             h->d_P.p, h->d_phi.p, h->d_psi.p, (int)c.size(), eta_dev, terms_dev, h->d_npts.p};
+             h->d_P.p, h->d_phi.p, h->d_psi.p, (int)c.size(),
+             1.0 / std::max(1, h->num.f_samples), eta_dev, terms_dev, h->d_npts.p};
   if (launch_reduce(rp, st) != 0) return cuda_fail(cudaGetLastError(), "reduce launch");
   cudaEventRecord(h->ev[3], st);
   launches += 1;

@@ -36,8 +36,10 @@ constexpr int LPT = LINE_CAP / BLOCK;  // lattice lines scanned per thread
 constexpr int CHAIN_MAX = ISRS_CHAIN_MAX;
 static_assert(LINE_CAP % BLOCK == 0, "LINE_CAP must be a multiple of BLOCK");
 
-// region flags (reading C8: a term whose gate or weight is zero is not evaluated)
-enum : int { NEED_E = 1, NEED_F = 2, NEED_G = 4, NEED_H = 8 };
+// region flags (reading C8: a term whose gate or weight is zero is not evaluated); bits >= 8
+// hold the index of the region's NLI frequency f in KParams::fv (COI centre, or one of the
+// f samples of the 3-D form)
+enum : int { NEED_E = 1, NEED_F = 2, NEED_G = 4, NEED_H = 8, FV_SHIFT = 8 };
 
 // MODE_SEG32: row a8, the mixed fp32 variant of the segment form (fp32 recurrence, mu, phase
 // factor; fp64 chi h and its exact reduction, the phase advance and every accumulation)
@@ -87,6 +89,7 @@ struct KParams {
   int tw;               // table rows resident (<= TW_MAX)
   int N;                // grid points per channel axis
   // regions
+  const double* fv;     // NLI frequencies (offsets) indexed by flags >> FV_SHIFT
   const RegionDesc* desc;
   double* partials;     // [n_regions][6]: D_w, E_w, F_w, G_w, H_w, n_points
   int mode;
@@ -103,6 +106,7 @@ struct RParams {
   const double* phi;
   const double* psi;
   int n_coi;
+  double inv_fs;             // 1 / (number of f samples per COI): 1 in the 2-D path
   double* eta;
   double* terms;             // may be null
   double* npts;              // [n_coi]

@@ -291,7 +291,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
   const int k1 = rd.k1, k2 = rd.k2, flags = rd.flags;
   const int N = p.N;
 
-  const double f = __ldg(p.f + rd.kappa);
+  const double f = __ldg(p.fv + (flags >> FV_SHIFT));          // NLI frequency (C1 / 3-D f_m)
   const double lo1 = __ldg(p.lo + k1), lo2 = __ldg(p.lo + k2);
   const double d1 = __ldg(p.delta + k1), d2 = __ldg(p.delta + k2);
   // lattice ratio a:b = R1:R2 (coprime); f3 = C + g (a m1 + b m2), exact in fp64 (reading C10)
@@ -804,7 +804,8 @@ __global__ void __launch_bounds__(BLOCK) reduce_kernel(const RParams p) {
   if (threadIdx.x == 0) {
     const int kappa = p.coi[ci];
     const double Pk = p.P[kappa];
-    const double scale = p.R[kappa] / (Pk * Pk * Pk);   // P_NLI = R G_NLI (C1); Eq. 11
+    // P_NLI = R G_NLI(f_kappa) (C1) or R mean_m G_NLI(f_m) (3-D, NEXT-3); Eq. 11
+    const double scale = p.R[kappa] / (Pk * Pk * Pk) * p.inv_fs;
     double e = 0.0;
     for (int k = 0; k < 5; ++k) {
       const double t = red[k][0] * scale;

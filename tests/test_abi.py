@@ -53,7 +53,7 @@ def test_strerror(abi):
 def _create(abi, link, **kw):
     pa = abi.ProblemArrays(link)
     n = abi.numerics(kw.get("grid_n", link.grid_n), kw.get("dz", 1000.0), kw.get("precision", 64),
-                     kw.get("mu_mode", 0))
+                     kw.get("mu_mode", 0), 0, kw.get("f_samples", 0))
     h = ctypes.c_void_p()
     rc = abi.get().isrs_egn_create(ctypes.byref(pa.struct), ctypes.byref(n), 0, ctypes.byref(h))
     return rc, abi.get().isrs_egn_last_error().decode(), h
@@ -68,6 +68,10 @@ def test_validation_errors_before_any_cuda(abi):
     assert rc == abi.EINVAL and "delta_z" in msg
     rc, msg, _ = _create(abi, l, precision=16)
     assert rc == abi.EUNSUPPORTED
+    rc, msg, _ = _create(abi, l, f_samples=-1)
+    assert rc == abi.EINVAL and "f_samples" in msg
+    rc, msg, _ = _create(abi, l, f_samples=3)          # 64 GBd / 6 is not an integer (R3)
+    assert rc == abi.EINVAL and "f_samples" in msg
     rc, msg, _ = _create(abi, l, precision=32, mu_mode=abi.MU_MACLAURIN)
     assert rc == abi.EUNSUPPORTED and "segment" in msg
     bad = l.with_(f_center_hz=l.f_center_hz + 0.25)

@@ -307,6 +307,36 @@ def test_P6_unit_link_raw_integrals():
         assert abs(isl[k] / R ** 3 - 7.0 / 12.0) < 1e-5
 
 
+def test_P14_unit_link_3d_D_exact_discrete():
+    # NEXT-3 (3-D form, Eqs. 17-21 integrate f over the COI band): single channel, Y := 1, n = N
+    # f samples.  With f_m on the same bin-centre lattice, f3 = f1 + f2 - f_m is a bin centre (no
+    # ties) and the island of f_m holds #{m1 + m2 - m in [0, N-1]} points; summing over m counts
+    # every anti-diagonal s with weight n(s) = min(s, 2N-2-s) + 1 twice, so
+    # mean_m D(f_m) = delta^2 sum_s n(s)^2 / N = (2/3) R^2 (1 + 1/(2 N^2))   (combinatorics, exact).
+    R = 48e9
+    for N in (8, 16, 32):
+        l = tiny_link(n_ch=1, rates_gbd=(48,), n_span=1, grid_n=N, fmts=("qpsk",))
+        c = egn.canonicalize(l)
+        fs = egn.coi_frequencies(c, 0, N)
+        D = np.mean([egn.region_islands(c, 0, 0, 0, "unit", f=f)[0]["D"] for f in fs])
+        assert abs(D / R ** 2 - 2.0 / 3.0 * (1.0 + 0.5 / N ** 2)) < 1e-14
+
+
+@pytest.mark.parametrize("fmt", ["qpsk", "16qam"])
+def test_P14_unit_link_3d_closed_form(fmt):
+    # continuous limit over the band (derivation in DESIGN.md P14): D(f) = 3/4 R^2 - f^2,
+    # E(f) = F(f) = G(f) = 7/12 R^3 - R f^2, H(f) = (3/4 R^2 - f^2)^2; averaged over f:
+    # 2/3 R^2, R^3/2, 9/20 R^4  ->  eta = 32/81 + 48/81 Phi + 4/45 Psi, reached at O(h^2).
+    phi, psi = wl.FORMATS[fmt]
+    errs = []
+    for N in (8, 16, 32):
+        l = tiny_link(n_ch=1, rates_gbd=(48,), n_span=1, grid_n=N, fmts=(fmt,))
+        e, _ = egn.eta(l, mu_mode="unit", f_samples=N)
+        errs.append(abs(e[0] - egn.unit_link_eta_3d(phi, psi)))
+    assert errs[-1] < 1e-3
+    assert 3.5 < errs[0] / errs[1] < 4.5 and 3.5 < errs[1] / errs[2] < 4.5, errs
+
+
 def test_P10_grid_convergence_order_two():
     # single 10 GBd channel, 1 span: successive differences fall ~4x per halving of delta (midpoint rule)
     vals = []

@@ -182,6 +182,35 @@ def test_span_chaining_matches_unchained(isrs, cfg, coi):
     assert np.all(np.abs(ta - tb) <= TOL_ETA * np.abs(tb).sum(axis=1, keepdims=True))
 
 
+@pytest.mark.parametrize("name", ["uniform_64gbd_2span", "three_islands_96gbd", "mixed_rates_guard",
+                                  "touching_bands", "random_spans_multiclass"])
+def test_eta_parity_3d_tiny(isrs, name):
+    """NEXT-3: the 3-D form (f over the COI band, 4 midpoint samples) against the oracle."""
+    link = tiny_link(**TINY[name])
+    e_o, t_o = egn.eta(link, f_samples=4)
+    e_g, t_g = gpu_eta(isrs, link, f_samples=4)
+    assert np.all(np.abs(e_g - e_o) / e_o <= TOL_ETA), (name, np.abs(e_g - e_o) / e_o)
+    scale = np.abs(t_o).sum(axis=1, keepdims=True)
+    assert np.all(np.abs(t_g - t_o) <= TOL_ETA * scale)
+
+
+def test_eta_parity_3d_c1(isrs):
+    link = bj_config("c1")
+    e_o, _ = egn.eta(link, coi=[0, 2], f_samples=4)
+    e_g, _ = gpu_eta(isrs, link, coi=[0, 2], f_samples=4)
+    assert np.all(np.abs(e_g - e_o) / e_o <= TOL_ETA), (e_g, e_o)
+
+
+def test_unit_link_3d_through_cuda(isrs):
+    # pin P14 through the CUDA path: D exact (2/3 R^2 (1 + 1/(2N^2))), eta -> 32/81 + 48/81 Phi + 4/45 Psi
+    link = tiny_link(n_ch=1, rates_gbd=(48,), n_span=1, grid_n=32, fmts=("qpsk",))
+    e_g, t_g = gpu_eta(isrs, link, flags=isrs.FLAG_UNIT_LINK, f_samples=32)
+    e_o, t_o = egn.eta(link, mu_mode="unit", f_samples=32)
+    assert abs(e_g[0] - e_o[0]) <= 1e-13 and np.all(np.abs(t_g - t_o) <= 1e-13)
+    assert abs(t_g[0, 0] - 16.0 / 27.0 * 2.0 / 3.0 * (1.0 + 0.5 / 32 ** 2)) < 1e-13
+    assert abs(e_g[0] - egn.unit_link_eta_3d(-1.0, 4.0)) < 2e-3
+
+
 DB_TOL_FP32 = 1e-3     # north star: optional fp32 path within 0.001 dB
 
 

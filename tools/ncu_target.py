@@ -19,13 +19,15 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--coi", default=None)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--precision", type=int, default=64)
+    ap.add_argument("--f-samples", type=int, default=0)
     a = ap.parse_args()
     import torch
     import paper_2412_11614_b200 as isrs
     from workloads import bj_config
     link = bj_config(a.config)
     coi = [int(x) for x in a.coi.split(",")] if a.coi else None
-    with isrs.Engine(link) as e:
+    with isrs.Engine(link, precision=a.precision, f_samples=a.f_samples) as e:
         for _ in range(a.reps):
             eta = e.nli(coi=coi)
         torch.cuda.synchronize()
