@@ -5,9 +5,11 @@
 
 One step = one pass of the whole hot path (rows a2-a7: the nli() call: integrand kernels over
 every region of every COI + per-COI assembly) over BASELINE.json configs[1] (c2: C-band 40 x
-64 GBd, 10 x 80 km, N = 128, all 40 channels as COI), inputs resident in HBM.  The path
-partitions into independent links / COI sets; at N GPUs every rank evaluates its own copy of
-the link (weak scaling, no collective on the data path).
+64 GBd, 10 x 80 km, N = 128, all 40 channels as COI), inputs resident in HBM.  At N GPUs
+(torchrun, one process per GPU) the canonical region list is split into N cost-balanced
+contiguous shards; each rank evaluates its shard, the per-COI sums (n_ch x 6 fp64) are
+all-gathered over NCCL and combined in fixed rank order: strong scaling of one
+link, the same eta on every rank.
 
 Prints ONE JSON line (rank 0).  value = integrand point-spans/s over all ranks; the other parts
 of the BASELINE metric (channels/s, % of FP64 peak) are extra keys and in `roofline`.
@@ -176,7 +178,7 @@ def run_reference(args, link, ws, rank):
     value = pspans_tot / sum(per_step)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
             "steps": steps, "warmup": warm, "ms_per_step": 1e3 * float(np.mean(per_step)),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": config_desc(link, args),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": desc + " per step"},
@@ -190,7 +192,9 @@ def config_desc(link, args):
             "n_ch": link.n_ch, "n_span": link.n_span, "grid_n": link.grid_n,
             "n_coi": link.n_ch, "seed": link.seed,
             "l2": "flushed between timed steps (256 MiB write, outside the step events)",
-            "parallelism": f"replicas x{args.gpus} (independent links, weak scaling)"}
+            "parallelism": (f"region shards x{args.gpus} (cost-balanced contiguous shards of one link, "
+                            "NCCL all-gather of per-COI sums, fixed-order combine; strong scaling)"
+                            if args.gpus > 1 else "1 GPU")}
 
 
 def run_ours(args, link, ws, rank, local):
@@ -205,16 +209,34 @@ def run_ours(args, link, ws, rank, local):
     terms = torch.empty((n, 5), dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    def step():
-        eng.nli_into(eta.data_ptr(), terms.data_ptr(), None, stream.cuda_stream)
+    if ws > 1:
+        # rank r evaluates shard r of the canonical region list (cost-balanced), the
+        # per-COI sums [n, 6] are all-gathered over NCCL (NVLink/NVSwitch) and every rank combines
+        # them in fixed rank order -> the same eta on every rank (strong scaling of one link).
+        import torch.distributed as dist
+        sums = torch.empty((n, 6), dtype=torch.float64, device=dev)
+        gathered = torch.empty((ws, n, 6), dtype=torch.float64, device=dev)
+
+        def step():
+            eng.nli_shard_into(rank, ws, sums.data_ptr(), None, stream.cuda_stream)
+            dist.all_gather_into_tensor(gathered, sums)
+            eng.combine_into(ws, gathered.data_ptr(), eta.data_ptr(), terms.data_ptr(), None,
+                             stream.cuda_stream)
+    else:
+        def step():
+            eng.nli_into(eta.data_ptr(), terms.data_ptr(), None, stream.cuda_stream)
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             flush.zero_()
             step()
     torch.cuda.synchronize()
-    pts, pspans, nreg = eng.work()
-    launches_per_step = eng.last_launch_count()
+    pts, pspans, nreg = eng.work()          # this rank's share
+    launches_per_step = eng.last_launch_count() + (1 if ws > 1 else 0)
+    if ws > 1:
+        tot = torch.tensor([pts, pspans, nreg], dtype=torch.int64, device=dev)
+        torch.distributed.all_reduce(tot)
+        pts, pspans, nreg = (int(v) for v in tot.tolist())
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
@@ -264,21 +286,35 @@ def run_ours(args, link, ws, rank, local):
         h2d = pa.nbytes()
         t_e2e = []
         for k in range(max(1, min(3, args.steps))):
+            if ws > 1:
+                torch.distributed.barrier()
             t0 = time.perf_counter()
-            isrs.eta_host(link, device=local, precision=args.precision)
-            t_e2e.append(time.perf_counter() - t0)
-        e2e = {"value": ws * pspans / float(np.median(t_e2e)), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            if ws > 1:
+                with isrs.Engine(link, device=local, precision=args.precision) as e2:
+                    s2 = e2.nli_shard(rank, ws)
+                    g2 = torch.empty((ws, n, 6), dtype=torch.float64, device=dev)
+                    torch.distributed.all_gather_into_tensor(g2, s2)
+                    e2.combine(g2).cpu()
+            else:
+                isrs.eta_host(link, device=local, precision=args.precision)
+            dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+            if ws > 1:
+                torch.distributed.all_reduce(dt, op=torch.distributed.ReduceOp.MAX)
+            t_e2e.append(float(dt.item()))
+        e2e = {"value": pspans / float(np.median(t_e2e)), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 8 * n,
-               "note": "isrs_egn_eta_host(): validate + region plan + H2D + precompute + nli + D2H + free"}
+               "note": ("isrs_egn_eta_host(): validate + region plan + H2D + precompute + nli + D2H + free"
+                        if ws == 1 else "per rank: create (H2D, precompute) + nli_shard + NCCL all-gather "
+                        "+ combine + D2H + destroy; max over ranks")}
 
     if rank == 0:
-        value = ws * pspans / (ms_max * 1e-3)
+        value = pspans / (ms_max * 1e-3)          # the whole link's point-spans over all ranks
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None,
+                "scaling": "strong", "vs_baseline": None,
                 "dtype": "f64" if args.precision == 64 else "f32 (mixed, row a8)", "data": "synthetic",
                 "config": config_desc(link, args),
-                "channels_per_s": ws * n / (ms_max * 1e-3),
+                "channels_per_s": n / (ms_max * 1e-3),
                 "point_spans_per_step": pspans, "points_per_step": pts, "regions_per_step": nreg,
                 "kernel_ms": {"integrand_D": kd_ms, "integrand_coherent": kc_ms, "reduce": kr_ms},
                 "roofline": {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
@@ -296,7 +332,7 @@ def run_ours(args, link, ws, rank, local):
                 "gpu_launches": launches_per_step * args.steps,
                 "clocks": clk, "e2e": e2e,
                 "eta_db_first_mid_last": [float(10 * np.log10(eta_host[i])) for i in (0, n // 2, n - 1)]}
-        if not args.no_cpu:
+        if not args.no_cpu and ws == 1:
             rate, ps, dt, cores, desc = oracle_sample(link, args.cpu_seconds)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                                     "sample": f"{desc}; {ps} point-spans in {dt:.1f} s"}

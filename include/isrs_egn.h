@@ -98,6 +98,26 @@ ISRS_EGN_API int isrs_egn_create(const isrs_egn_problem *p, const isrs_egn_numer
 ISRS_EGN_API int isrs_egn_nli(isrs_egn_t *h, int32_t n_coi, const int32_t *coi, double *eta_dev,
                  double *terms_dev, void *cuda_stream);
 
+/* ---- Multi-GPU: one process and one handle per GPU.  The canonical region list of
+ * the COI set (COI, f sample, k1, k2 order) is split into `world` contiguous shards of near-equal cost
+ * (in-support points); shard `rank` is evaluated and the per-COI sums of its regions, BEFORE the
+ * Eq. 11 scale, are written to coi_sums_dev (DEVICE [n_coi * 6]: Eq. 15-weighted D, E, F, G, H sums and
+ * the point count).  The caller all-gathers them into [world][n_coi][6] (e.g. ncclAllGather) and calls
+ * isrs_egn_combine, which adds them in fixed rank order and scales: the same eta on every rank, bitwise.
+ * Asynchronous on cuda_stream like isrs_egn_nli. */
+ISRS_EGN_API int isrs_egn_nli_shard(isrs_egn_t *h, int32_t n_coi, const int32_t *coi, int32_t rank,
+                                    int32_t world, double *coi_sums_dev, void *cuda_stream);
+/* eta_dev [n_coi] (and terms_dev [n_coi * 5] or NULL) from gathered_dev [world][n_coi][6] (DEVICE).
+ * coi must be the COI set of the preceding isrs_egn_nli_shard call on this handle. */
+ISRS_EGN_API int isrs_egn_combine(isrs_egn_t *h, int32_t n_coi, const int32_t *coi, int32_t world,
+                                  const double *gathered_dev, double *eta_dev, double *terms_dev,
+                                  void *cuda_stream);
+/* Host-only planner query (touches no device): for each rank r < world, the number of regions,
+ * in-support points and first canonical region index of its shard (each array [world] or NULL). */
+ISRS_EGN_API int isrs_egn_plan_shards(const isrs_egn_problem *p, const isrs_egn_numerics *n, int32_t n_coi,
+                                      const int32_t *coi, int32_t world, int64_t *regions_out,
+                                      int64_t *points_out, int64_t *first_region_out);
+
 /* Per-region partial integrals written by the most recent isrs_egn_nli() call (synchronises
  * the handle's last stream).  For each query q: region (kappa[q], k1[q], k2[q]) ->
  * out_host[6q .. 6q+5] = { D_w, E_w, F_w, G_w, H_w, n_points } with
@@ -109,8 +129,9 @@ ISRS_EGN_API int isrs_egn_nli(isrs_egn_t *h, int32_t n_coi, const int32_t *coi, 
 ISRS_EGN_API int isrs_egn_region_partials(isrs_egn_t *h, int32_t n, const int32_t *kappa, const int32_t *k1,
                              const int32_t *k2, double *out_host);
 
-/* Work of the most recent isrs_egn_nli() call (synchronises): in-support grid points summed
- * over COIs and regions, point-spans = points * n_span, and the number of regions launched. */
+/* Work of the most recent isrs_egn_nli() / isrs_egn_nli_shard() call (synchronises): in-support
+ * grid points summed over the regions it launched, point-spans = points * n_span, and the number
+ * of regions launched. */
 ISRS_EGN_API int isrs_egn_work(isrs_egn_t *h, int64_t *points, int64_t *point_spans, int64_t *regions);
 
 /* One-shot end-to-end call with HOST buffers: create + nli (all given COIs) + copy back +

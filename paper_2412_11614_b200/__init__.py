@@ -16,7 +16,7 @@ from . import _abi
 from ._abi import (FLAG_NO_CHAIN, FLAG_UNIT_LINK, MU_MACLAURIN, MU_SEGMENT, IsrsEgnError, ProblemArrays,  # noqa: F401
                    numerics)
 
-__all__ = ["Engine", "eta_host", "IsrsEgnError", "MU_SEGMENT", "MU_MACLAURIN", "FLAG_UNIT_LINK", "FLAG_NO_CHAIN",
+__all__ = ["Engine", "eta_host", "plan_shards", "IsrsEgnError", "MU_SEGMENT", "MU_MACLAURIN", "FLAG_UNIT_LINK", "FLAG_NO_CHAIN",
            "library_path"]
 
 
@@ -92,6 +92,47 @@ class Engine:
         _abi.check(_abi.get().isrs_egn_last_kernel_ms(self._h, ms, ps))
         return list(ms), list(ps)
 
+    def _coi(self, coi):
+        if coi is None:
+            return self.n_ch, None
+        c = np.ascontiguousarray(np.asarray(coi, dtype=np.int32))
+        self._coi_keep = c
+        return len(c), c.ctypes.data_as(_abi._ip)
+
+    def nli_shard_into(self, rank, world, sums_ptr, coi=None, stream=0):
+        """Multi-GPU shard (isrs_egn_nli_shard): per-COI sums [n_coi, 6] of shard `rank` of `world`."""
+        n, cp = self._coi(coi)
+        _abi.check(_abi.get().isrs_egn_nli_shard(self._h, n, cp, int(rank), int(world),
+                                               ctypes.c_void_p(sums_ptr), ctypes.c_void_p(stream or None)))
+
+    def combine_into(self, world, gathered_ptr, eta_ptr, terms_ptr=0, coi=None, stream=0):
+        """eta from all-gathered shard sums [world, n_coi, 6] (isrs_egn_combine, fixed rank order)."""
+        n, cp = self._coi(coi)
+        _abi.check(_abi.get().isrs_egn_combine(self._h, n, cp, int(world), ctypes.c_void_p(gathered_ptr),
+                                             ctypes.c_void_p(eta_ptr), ctypes.c_void_p(terms_ptr or None),
+                                             ctypes.c_void_p(stream or None)))
+
+    def nli_shard(self, rank, world, coi=None, stream=None):
+        import torch
+        n = self.n_ch if coi is None else len(coi)
+        dev = torch.device("cuda", self.device)
+        out = torch.empty((n, 6), dtype=torch.float64, device=dev)
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        self.nli_shard_into(rank, world, out.data_ptr(), coi, st.cuda_stream)
+        return out
+
+    def combine(self, gathered, coi=None, terms=False, stream=None):
+        import torch
+        world = gathered.shape[0]
+        n = gathered.shape[1]
+        g = gathered.contiguous()
+        eta = torch.empty(n, dtype=torch.float64, device=g.device)
+        tt = torch.empty((n, 5), dtype=torch.float64, device=g.device) if terms else None
+        st = stream if stream is not None else torch.cuda.current_stream(g.device)
+        self.combine_into(world, g.data_ptr(), eta.data_ptr(), tt.data_ptr() if terms else 0, coi,
+                          st.cuda_stream)
+        return (eta, tt) if terms else eta
+
     def span_chains(self):
         """(chain sizes G_c, K_s per span) of the handle's span chains (reading R9)."""
         n = ctypes.c_int32()
@@ -120,6 +161,26 @@ class Engine:
             self.close()
         except Exception:
             pass
+
+
+def plan_shards(link, world, coi=None, grid_n=None, delta_z_m=None, f_samples=0):
+    """Host-only shard plan (isrs_egn_plan_shards): (regions, points, first_region) arrays [world]."""
+    pa = ProblemArrays(link)
+    n = numerics(grid_n if grid_n is not None else link.grid_n,
+                 delta_z_m if delta_z_m is not None else getattr(link, "delta_z_m", 1000.0),
+                 64, MU_SEGMENT, 0, f_samples)
+    if coi is None:
+        nco, cp = pa.struct.n_ch, None
+    else:
+        c = np.ascontiguousarray(np.asarray(coi, dtype=np.int32))
+        nco, cp = len(c), c.ctypes.data_as(_abi._ip)
+    r = np.zeros(world, dtype=np.int64)
+    p = np.zeros(world, dtype=np.int64)
+    f = np.zeros(world, dtype=np.int64)
+    _abi.check(_abi.get().isrs_egn_plan_shards(ctypes.byref(pa.struct), ctypes.byref(n), nco, cp, int(world),
+                                             r.ctypes.data_as(_abi._lp), p.ctypes.data_as(_abi._lp),
+                                             f.ctypes.data_as(_abi._lp)))
+    return r, p, f
 
 
 def eta_host(link, coi=None, grid_n=None, delta_z_m=None, device=0, precision=64, mu_mode=MU_SEGMENT,

@@ -19,7 +19,7 @@ FLAG_NO_CHAIN = 2
 
 EXPORTED = ("isrs_egn_create", "isrs_egn_nli", "isrs_egn_region_partials", "isrs_egn_work",
             "isrs_egn_eta_host", "isrs_egn_last_kernel_ms", "isrs_egn_last_launch_count",
-            "isrs_egn_span_chains",
+            "isrs_egn_span_chains", "isrs_egn_nli_shard", "isrs_egn_combine", "isrs_egn_plan_shards",
             "isrs_egn_destroy",
             "isrs_egn_strerror", "isrs_egn_last_error")
 
@@ -68,6 +68,15 @@ def _load():
     lib.isrs_egn_eta_host.restype = ctypes.c_int
     lib.isrs_egn_last_kernel_ms.argtypes = [ctypes.c_void_p, _dp, _dp]
     lib.isrs_egn_last_kernel_ms.restype = ctypes.c_int
+    lib.isrs_egn_nli_shard.argtypes = [ctypes.c_void_p, ctypes.c_int32, _ip, ctypes.c_int32, ctypes.c_int32,
+                                       ctypes.c_void_p, ctypes.c_void_p]
+    lib.isrs_egn_nli_shard.restype = ctypes.c_int
+    lib.isrs_egn_combine.argtypes = [ctypes.c_void_p, ctypes.c_int32, _ip, ctypes.c_int32, ctypes.c_void_p,
+                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    lib.isrs_egn_combine.restype = ctypes.c_int
+    lib.isrs_egn_plan_shards.argtypes = [ctypes.POINTER(Problem), ctypes.POINTER(Numerics), ctypes.c_int32, _ip,
+                                         ctypes.c_int32, _lp, _lp, _lp]
+    lib.isrs_egn_plan_shards.restype = ctypes.c_int
     lib.isrs_egn_span_chains.argtypes = [ctypes.c_void_p, _ip, _ip, _ip]
     lib.isrs_egn_span_chains.restype = ctypes.c_int
     lib.isrs_egn_last_launch_count.argtypes = [ctypes.c_void_p]

@@ -59,6 +59,7 @@ struct DevBuf {
 };
 
 struct WorkList {
+  std::vector<long long> cost;   // in-support points per region (canonical order)
   std::vector<int> coi;
   std::vector<double> fv;   // NLI frequency of each (COI, f sample)
   std::vector<RegionDesc> desc;
@@ -92,6 +93,11 @@ struct isrs_egn {
   DevBuf<long long> d_coi_off;
   DevBuf<int> d_coi, d_list_d, d_list_c;
   DevBuf<double> d_fv;
+  // regions launched by the last call (the whole list, or one shard of it)
+  std::vector<int> act_d, act_c;
+  int sh_rank = -1, sh_world = -1;
+  long long sh_lo = 0, sh_hi = 0;
+  DevBuf<int> d_sh_d, d_sh_c;
   DevBuf<double> d_partials, d_npts;
   cudaStream_t last_stream = nullptr;
   bool have_result = false;
@@ -169,25 +175,14 @@ static int cuda_fail(cudaError_t e, const char* what) {
   return fail(ISRS_EGN_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numerics* n, int device,
-                               isrs_egn_t** out) {
-  if (!out) return fail(ISRS_EGN_EINVAL, "out is NULL");
-  *out = nullptr;
-  isrs_egn_numerics num = n ? *n : isrs_egn_numerics{};
-  if (num.precision == 0) num.precision = 64;
-  int rc = validate(p, &num);
-  if (rc) return rc;
-  cudaError_t ce = cudaSetDevice(device);
-  if (ce != cudaSuccess) return cuda_fail(ce, "cudaSetDevice");
-
-  auto* h = new isrs_egn();
-  h->device = device;
+// Host-side canonicalisation of the channel plan (reading C5): offsets from the occupied-band
+// midpoint f_c, B_tot edge-to-edge, P_tot = sum P_i, G_i = P_i / R_i, delta_i = R_i / N.
+static void canon_channels(isrs_egn* h, const isrs_egn_problem* p, const isrs_egn_numerics& num) {
   h->num = num;
   h->n_ch = p->n_ch;
   h->n_span = p->n_span;
   h->N = num.grid_n;
   const int nc = p->n_ch, N = num.grid_n;
-  // ---- canonicalisation (reading C5)
   double lo_min = 1e300, hi_max = -1e300;
   for (int i = 0; i < nc; ++i) {
     lo_min = std::min(lo_min, p->f_center_hz[i] - p->symbol_rate_hz[i] / 2);
@@ -210,6 +205,23 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
     h->rate.push_back((long long)R);
     h->p_tot += p->launch_power_w[i];
   }
+}
+
+extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numerics* n, int device,
+                               isrs_egn_t** out) {
+  if (!out) return fail(ISRS_EGN_EINVAL, "out is NULL");
+  *out = nullptr;
+  isrs_egn_numerics num = n ? *n : isrs_egn_numerics{};
+  if (num.precision == 0) num.precision = 64;
+  int rc = validate(p, &num);
+  if (rc) return rc;
+  cudaError_t ce = cudaSetDevice(device);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaSetDevice");
+
+  auto* h = new isrs_egn();
+  h->device = device;
+  canon_channels(h, p, num);
+  const int N = num.grid_n;
   // ---- spans and classes
   std::map<std::tuple<double, double, double>, int> cls_of;
   std::vector<double> cL, cA, cC;
@@ -254,16 +266,20 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
   // gamma, C_r, hence the same z = e^{i chi h} and envelope table) with an even K_s share one
   // recurrence over G * K_s segments, G * K_s <= CHAIN_MAX.  Segment mode only.
   std::vector<int> ch_s0, ch_g;
-  const bool chain_ok = num.mu_mode == ISRS_EGN_MU_SEGMENT && num.precision == 64 &&
+  // precision 32 (row a8): runs of identical spans share z, I_0 and the per-span phase step
+  // (common subexpressions), but every span keeps its own K-segment recurrence; cap 1024 spans
+  const bool chain_ok = num.mu_mode == ISRS_EGN_MU_SEGMENT &&
                         !(num.flags & (ISRS_EGN_FLAG_NO_CHAIN | ISRS_EGN_FLAG_UNIT_LINK));
+  const long long chain_cap = (num.precision == 32) ? 1024LL * 1000000 : CHAIN_MAX;
   for (int s = 0; s < p->n_span; ++s) {
-    const bool same = s > 0 && chain_ok && (K[s] % 2 == 0) && p->length_m[s] == p->length_m[s - 1] &&
+    const bool same = s > 0 && chain_ok && (num.precision == 32 || K[s] % 2 == 0) &&
+                      p->length_m[s] == p->length_m[s - 1] &&
                       p->alpha_per_m[s] == p->alpha_per_m[s - 1] &&
                       p->beta2_s2_per_m[s] == p->beta2_s2_per_m[s - 1] &&
                       p->beta3_s3_per_m[s] == p->beta3_s3_per_m[s - 1] &&
                       p->gamma_per_w_m[s] == p->gamma_per_w_m[s - 1] &&
                       p->cr_per_w_m_hz[s] == p->cr_per_w_m_hz[s - 1] &&
-                      (long long)(ch_g.back() + 1) * K[s] <= CHAIN_MAX;
+                      (long long)(ch_g.back() + 1) * (num.precision == 32 ? 1000000 : K[s]) <= chain_cap;
     if (same) {
       ch_g.back() += 1;
     } else {
@@ -371,7 +387,8 @@ static void build_worklist(const isrs_egn* h, const std::vector<int>& coi, WorkL
   w->coi_off.assign(1, 0);
   w->list_d.clear();
   w->list_c.clear();
-  std::vector<long long> cost;
+  std::vector<long long>& cost = w->cost;
+  cost.clear();
   const int nc = h->n_ch;
   const int fs = h->num.f_samples, nfs = std::max(1, fs);
   for (int kappa : coi) {
@@ -411,27 +428,50 @@ static void build_worklist(const isrs_egn* h, const std::vector<int>& coi, WorkL
   std::stable_sort(w->list_c.begin(), w->list_c.end(), by_cost);
 }
 
-extern "C" int isrs_egn_nli(isrs_egn_t* h, int32_t n_coi, const int32_t* coi, double* eta_dev,
-                            double* terms_dev, void* cuda_stream) {
-  if (!h) return fail(ISRS_EGN_EINVAL, "handle is NULL");
-  if (!eta_dev) return fail(ISRS_EGN_EINVAL, "eta_dev is NULL");
-  std::vector<int> c;
+static int coi_list(const isrs_egn* h, int32_t n_coi, const int32_t* coi, std::vector<int>* c) {
+  c->clear();
   if (!coi) {
     if (n_coi != h->n_ch) return fail(ISRS_EGN_EINVAL, "coi == NULL requires n_coi == n_ch");
-    for (int i = 0; i < h->n_ch; ++i) c.push_back(i);
-  } else {
-    if (n_coi < 1) return fail(ISRS_EGN_EINVAL, "n_coi < 1");
-    for (int i = 0; i < n_coi; ++i) {
-      if (coi[i] < 0 || coi[i] >= h->n_ch)
-        return fail(ISRS_EGN_EINVAL, "coi[" + std::to_string(i) + "] out of range");
-      c.push_back(coi[i]);
-    }
+    for (int i = 0; i < h->n_ch; ++i) c->push_back(i);
+    return ISRS_EGN_OK;
   }
+  if (n_coi < 1) return fail(ISRS_EGN_EINVAL, "n_coi < 1");
+  for (int i = 0; i < n_coi; ++i) {
+    if (coi[i] < 0 || coi[i] >= h->n_ch)
+      return fail(ISRS_EGN_EINVAL, "coi[" + std::to_string(i) + "] out of range");
+    c->push_back(coi[i]);
+  }
+  return ISRS_EGN_OK;
+}
+
+// Shard `rank` of `world`: the contiguous canonical region range whose cumulative
+// cost (points) lies in [rank, rank + 1) * total / world.  world = 1 -> everything.
+static void shard_range(const WorkList& w, int rank, int world, long long* lo, long long* hi) {
+  const long long n = (long long)w.cost.size();
+  if (world <= 1) {
+    *lo = 0;
+    *hi = n;
+    return;
+  }
+  long double tot = 0;
+  for (long long v : w.cost) tot += (long double)v + 1;   // +1: empty regions still cost a CTA
+  const long double a = tot * rank / world, b = tot * (rank + 1) / world;
+  long double acc = 0;
+  long long i = 0;
+  while (i < n && acc + 0.5L * ((long double)w.cost[i] + 1) < a) acc += (long double)w.cost[i++] + 1;
+  *lo = i;
+  while (i < n && acc + 0.5L * ((long double)w.cost[i] + 1) < b) acc += (long double)w.cost[i++] + 1;
+  *hi = (rank == world - 1) ? n : i;
+}
+
+// The hot path: integrand over the regions of shard (rank, world) of the COI set, then either the
+// per-COI assembly into eta (part_out == NULL; world must be 1) or the raw per-COI sums.
+static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, double* eta_dev,
+                   double* terms_dev, double* part_out, cudaStream_t st) {
   cudaError_t ce = cudaSetDevice(h->device);
   if (ce != cudaSuccess) return cuda_fail(ce, "cudaSetDevice");
   ce = cudaGetLastError();
   if (ce != cudaSuccess) return cuda_fail(ce, "pending CUDA error");
-  cudaStream_t st = (cudaStream_t)cuda_stream;
   if (!(h->have_result || h->wl.desc.size()) || h->wl.coi != c) {
     // (re)build and upload the work list for this COI set (cached across identical calls)
     cudaStreamSynchronize(h->last_stream);
@@ -442,6 +482,33 @@ extern "C" int isrs_egn_nli(isrs_egn_t* h, int32_t n_coi, const int32_t* coi, do
               h->d_partials.alloc(h->wl.desc.size() * 6) &&
               h->d_npts.alloc(c.size());
     if (!ok) return fail(ISRS_EGN_ENOMEM, "work-list allocation failed");
+    h->sh_rank = h->sh_world = -1;
+  }
+  const int* dl_d = h->d_list_d.p;
+  const int* dl_c = h->d_list_c.p;
+  long long r_lo = 0, r_hi = (long long)h->wl.desc.size();
+  if (world > 1) {
+    if (h->sh_rank != rank || h->sh_world != world) {
+      cudaStreamSynchronize(h->last_stream);
+      shard_range(h->wl, rank, world, &h->sh_lo, &h->sh_hi);
+      h->act_d.clear();
+      h->act_c.clear();
+      for (int id : h->wl.list_d)
+        if (id >= h->sh_lo && id < h->sh_hi) h->act_d.push_back(id);
+      for (int id : h->wl.list_c)
+        if (id >= h->sh_lo && id < h->sh_hi) h->act_c.push_back(id);
+      if (!h->d_sh_d.upload(h->act_d) || !h->d_sh_c.upload(h->act_c))
+        return fail(ISRS_EGN_ENOMEM, "shard list allocation failed");
+      h->sh_rank = rank;
+      h->sh_world = world;
+    }
+    dl_d = h->d_sh_d.p;
+    dl_c = h->d_sh_c.p;
+    r_lo = h->sh_lo;
+    r_hi = h->sh_hi;
+  } else {
+    h->act_d = h->wl.list_d;
+    h->act_c = h->wl.list_c;
   }
   KParams kp{};
   kp.lo = h->d_lo.p; kp.hi = h->d_hi.p; kp.f = h->d_f.p; kp.G = h->d_G.p; kp.R = h->d_R.p;
@@ -463,23 +530,90 @@ extern "C" int isrs_egn_nli(isrs_egn_t* h, int32_t n_coi, const int32_t* coi, do
   }
   int launches = 0;
   cudaEventRecord(h->ev[0], st);
-  if (launch_integrand(kp, h->d_list_d.p, (long long)h->wl.list_d.size(), false, st, &launches) != 0)
+  if (launch_integrand(kp, dl_d, (long long)h->act_d.size(), false, st, &launches) != 0)
     return cuda_fail(cudaGetLastError(), "integrand launch (D-only regions)");
   cudaEventRecord(h->ev[1], st);
-  if (launch_integrand(kp, h->d_list_c.p, (long long)h->wl.list_c.size(), true, st, &launches) != 0)
+  if (launch_integrand(kp, dl_c, (long long)h->act_c.size(), true, st, &launches) != 0)
     return cuda_fail(cudaGetLastError(), "integrand launch (coherent regions)");
   cudaEventRecord(h->ev[2], st);
-  h->launched[0] = !h->wl.list_d.empty();
-  h->launched[1] = !h->wl.list_c.empty();
+  h->launched[0] = !h->act_d.empty();
+  h->launched[1] = !h->act_c.empty();
   RParams rp{h->d_desc.p, h->d_partials.p, h->d_coi_off.p, h->d_coi.p, h->d_G.p, h->d_R.p,
              h->d_P.p, h->d_phi.p, h->d_psi.p, (int)c.size(),
-             1.0 / std::max(1, h->num.f_samples), eta_dev, terms_dev, h->d_npts.p};
+             1.0 / std::max(1, h->num.f_samples), eta_dev, terms_dev, h->d_npts.p, r_lo, r_hi,
+             part_out};
   if (launch_reduce(rp, st) != 0) return cuda_fail(cudaGetLastError(), "reduce launch");
   cudaEventRecord(h->ev[3], st);
   launches += 1;
   h->last_launches = launches;
   h->last_stream = st;
   h->have_result = true;
+  return ISRS_EGN_OK;
+}
+
+extern "C" int isrs_egn_nli(isrs_egn_t* h, int32_t n_coi, const int32_t* coi, double* eta_dev,
+                            double* terms_dev, void* cuda_stream) {
+  if (!h) return fail(ISRS_EGN_EINVAL, "handle is NULL");
+  if (!eta_dev) return fail(ISRS_EGN_EINVAL, "eta_dev is NULL");
+  std::vector<int> c;
+  int rc = coi_list(h, n_coi, coi, &c);
+  if (rc) return rc;
+  return run_nli(h, c, 0, 1, eta_dev, terms_dev, nullptr, (cudaStream_t)cuda_stream);
+}
+
+extern "C" int isrs_egn_nli_shard(isrs_egn_t* h, int32_t n_coi, const int32_t* coi, int32_t rank,
+                                  int32_t world, double* coi_sums_dev, void* cuda_stream) {
+  if (!h) return fail(ISRS_EGN_EINVAL, "handle is NULL");
+  if (!coi_sums_dev) return fail(ISRS_EGN_EINVAL, "coi_sums_dev is NULL");
+  if (world < 1 || rank < 0 || rank >= world) return fail(ISRS_EGN_EINVAL, "rank/world out of range");
+  std::vector<int> c;
+  int rc = coi_list(h, n_coi, coi, &c);
+  if (rc) return rc;
+  return run_nli(h, c, rank, world, nullptr, nullptr, coi_sums_dev, (cudaStream_t)cuda_stream);
+}
+
+extern "C" int isrs_egn_combine(isrs_egn_t* h, int32_t n_coi, const int32_t* coi, int32_t world,
+                                const double* gathered_dev, double* eta_dev, double* terms_dev,
+                                void* cuda_stream) {
+  if (!h) return fail(ISRS_EGN_EINVAL, "handle is NULL");
+  if (!gathered_dev || !eta_dev) return fail(ISRS_EGN_EINVAL, "gathered_dev / eta_dev is NULL");
+  if (world < 1) return fail(ISRS_EGN_EINVAL, "world < 1");
+  std::vector<int> c;
+  int rc = coi_list(h, n_coi, coi, &c);
+  if (rc) return rc;
+  cudaError_t ce = cudaSetDevice(h->device);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaSetDevice");
+  if (h->wl.coi != c || !h->d_coi.p) return fail(ISRS_EGN_EINVAL, "combine: COI set differs from the last shard call");
+  CParams cp{gathered_dev, world, h->d_coi.p, h->d_R.p, h->d_P.p, (int)c.size(),
+             1.0 / std::max(1, h->num.f_samples), eta_dev, terms_dev, nullptr};
+  if (launch_combine(cp, cuda_stream) != 0) return cuda_fail(cudaGetLastError(), "combine launch");
+  return ISRS_EGN_OK;
+}
+
+extern "C" int isrs_egn_plan_shards(const isrs_egn_problem* p, const isrs_egn_numerics* n, int32_t n_coi,
+                                    const int32_t* coi, int32_t world, int64_t* regions_out,
+                                    int64_t* points_out, int64_t* first_region_out) {
+  isrs_egn_numerics num = n ? *n : isrs_egn_numerics{};
+  if (num.precision == 0) num.precision = 64;
+  int rc = validate(p, &num);
+  if (rc) return rc;
+  if (world < 1) return fail(ISRS_EGN_EINVAL, "world < 1");
+  isrs_egn h;                       // host-only: no device memory is touched
+  canon_channels(&h, p, num);
+  std::vector<int> c;
+  rc = coi_list(&h, n_coi, coi, &c);
+  if (rc) return rc;
+  WorkList w;
+  build_worklist(&h, c, &w);
+  for (int r = 0; r < world; ++r) {
+    long long lo, hi;
+    shard_range(w, r, world, &lo, &hi);
+    long long pts = 0;
+    for (long long i = lo; i < hi; ++i) pts += w.cost[i];
+    if (regions_out) regions_out[r] = hi - lo;
+    if (points_out) points_out[r] = pts;
+    if (first_region_out) first_region_out[r] = lo;
+  }
   return ISRS_EGN_OK;
 }
 
@@ -514,14 +648,17 @@ extern "C" int isrs_egn_work(isrs_egn_t* h, int64_t* points, int64_t* point_span
   if (!h->have_result) return fail(ISRS_EGN_EINVAL, "no isrs_egn_nli() result yet");
   cudaError_t ce = cudaStreamSynchronize(h->last_stream);
   if (ce != cudaSuccess) return cuda_fail(ce, "stream sync");
-  std::vector<double> np(h->wl.coi.size());
-  ce = cudaMemcpy(np.data(), h->d_npts.p, np.size() * sizeof(double), cudaMemcpyDeviceToHost);
+  const size_t nr = h->wl.desc.size();
+  std::vector<double> np(nr);
+  ce = cudaMemcpy2D(np.data(), sizeof(double), h->d_partials.p + 5, 6 * sizeof(double), sizeof(double), nr,
+                    cudaMemcpyDeviceToHost);
   if (ce != cudaSuccess) return cuda_fail(ce, "npts copy");
   long long tot = 0;
-  for (double v : np) tot += (long long)v;
+  for (int id : h->act_d) tot += (long long)np[id];
+  for (int id : h->act_c) tot += (long long)np[id];
   if (points) *points = tot;
   if (point_spans) *point_spans = tot * h->n_span;
-  if (regions) *regions = (long long)h->wl.desc.size();
+  if (regions) *regions = (long long)(h->act_d.size() + h->act_c.size());
   return ISRS_EGN_OK;
 }
 
@@ -542,8 +679,8 @@ extern "C" int isrs_egn_last_kernel_ms(isrs_egn_t* h, double* ms_out, double* po
                       sizeof(double), nr, cudaMemcpyDeviceToHost);
     if (ce != cudaSuccess) return cuda_fail(ce, "npts copy");
     double a = 0, b = 0;
-    for (int id : h->wl.list_d) a += np[id];
-    for (int id : h->wl.list_c) b += np[id];
+    for (int id : h->act_d) a += np[id];
+    for (int id : h->act_c) b += np[id];
     point_spans_out[0] = a * h->n_span;
     point_spans_out[1] = b * h->n_span;
     point_spans_out[2] = (a + b) * h->n_span;

@@ -110,6 +110,21 @@ struct RParams {
   double* eta;
   double* terms;             // may be null
   double* npts;              // [n_coi]
+  long long r_lo, r_hi;      // canonical region range summed (a shard; [0, inf) = all)
+  double* part_out;          // shard mode: raw per-COI sums [n_coi][6] instead of eta/terms/npts
+};
+
+struct CParams {             // combine gathered shard sums [world][n_coi][6] in rank order
+  const double* gathered;
+  int world;
+  const int* coi;
+  const double* R;
+  const double* P;
+  int n_coi;
+  double inv_fs;
+  double* eta;
+  double* terms;             // may be null
+  double* npts;              // may be null
 };
 
 struct PParams {  // precompute
@@ -130,5 +145,6 @@ int launch_precompute(const PParams& p, void* stream);
 int launch_integrand(const KParams& p, const int* list, long long n_list, bool coherent,
                      void* stream, int* n_launches);
 int launch_reduce(const RParams& p, void* stream);
+int launch_combine(const CParams& p, void* stream);
 
 }  // namespace isrs

@@ -487,62 +487,78 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
             const float4* rowq =
                 reinterpret_cast<const float4*>(reinterpret_cast<const float*>(sm.T) + (li - tb) * 2 * p.tstride);
             double xs[PPT];
-            float sf[PPT], cf[PPT];
-            float2 c2[PPT / 2], b1[PPT / 2], b2[PPT / 2];
+            float sf[PPT], cf[PPT], nrf[PPT], nif[PPT], prr[PPT], pri[PPT], drr[PPT], dri[PPT];
+            float2 c2[PPT / 2];
 #pragma unroll
             for (int q = 0; q < PPT; ++q) {
               xs[q] = uv[q] * fma(A3, Ssum[q], A2);                 // chi h / pi
               const double r = xs[q] - 2.0 * rint(0.5 * xs[q]);     // exact, |r| <= 1
               sincospif((float)r, &sf[q], &cf[q]);
-            }
-#pragma unroll
-            for (int hq = 0; hq < PPT / 2; ++hq) {
-              c2[hq] = make_float2(2.f * cf[2 * hq], 2.f * cf[2 * hq + 1]);
-              b1[hq] = make_float2(0.f, 0.f);
-              b2[hq] = make_float2(0.f, 0.f);
-            }
-            const float2 neg1 = make_float2(-1.f, -1.f);
-            auto step = [&](float a) {
-#pragma unroll
-              for (int hq = 0; hq < PPT / 2; ++hq) {
-                const float2 t = __ffma2_rn(b2[hq], neg1, make_float2(a, a));   // a - b_{k+2}
-                const float2 n = __ffma2_rn(c2[hq], b1[hq], t);
-                b2[hq] = b1[hq];
-                b1[hq] = n;
-              }
-            };
-            const int n4 = Kp4 >> 2;
-            float4 tc = rowq[0];
-#pragma unroll 2
-            for (int i4 = 0; i4 < n4 - 1; ++i4) {
-              const float4 tn = rowq[i4 + 1];
-              step(tc.x);
-              step(tc.y);
-              step(tc.z);
-              step(tc.w);
-              tc = tn;
-            }
-            step(tc.x);
-            step(tc.y);
-            step(tc.z);                                             // -> b_1, b_2
-#pragma unroll
-            for (int q = 0; q < PPT; ++q) {
-              const float bb1 = (q & 1) ? b1[q >> 1].y : b1[q >> 1].x;
-              const float bb2 = (q & 1) ? b2[q >> 1].y : b2[q >> 1].x;
-              const float accr = fmaf(cf[q], bb1, tc.w - bb2);       // a'_0 + z b_1 - b_2
-              const float acci = sf[q] * bb1;
+              // I_0 = (w - 1)/(i chi - alpha): the same for every span of the run (G identical spans)
               const float px = (float)(CUDART_PI * xs[q]);
               const float wr1 = fmaf(Ehf, cf[q], -1.f), wi = Ehf * sf[q];
               const float inv = __fdividef(ghf, fmaf(px, px, ahf * ahf));
-              const float nr = fmaf(wi, px, -ahf * wr1);
-              const float ni = -fmaf(px, wr1, ahf * wi);
-              const float mr = (nr * accr - ni * acci) * inv;
-              const float mi = (nr * acci + ni * accr) * inv;
-              float ps = 0.f, pc = 1.f;
-              if (ch > 0) __sincosf(CUDART_PI_F * (float)th[q], &ps, &pc);
-              yr[q] += (double)fmaf(mr, pc, -mi * ps);
-              yi[q] += (double)fmaf(mr, ps, mi * pc);
-              const double t2 = fma(xs[q], (double)Ks, th[q]);
+              nrf[q] = fmaf(wi, px, -ahf * wr1) * inv;
+              nif[q] = -fmaf(px, wr1, ahf * wi) * inv;
+              // span phase e^{i theta_s} and its per-span step e^{i chi L} (reading C3)
+              const double tk = xs[q] * Ks;
+              const double rk = tk - 2.0 * rint(0.5 * tk);
+              sincospif((float)rk, &dri[q], &drr[q]);
+              if (ch > 0) __sincosf(CUDART_PI_F * (float)th[q], &pri[q], &prr[q]);
+              else { pri[q] = 0.f; prr[q] = 1.f; }
+            }
+#pragma unroll
+            for (int hq = 0; hq < PPT / 2; ++hq) c2[hq] = make_float2(2.f * cf[2 * hq], 2.f * cf[2 * hq + 1]);
+            const float2 neg1 = make_float2(-1.f, -1.f);
+            const int n4 = Kp4 >> 2;
+            for (int gi = 0; gi < G; ++gi) {
+              // ---- each span's own K-segment recurrence (Eqs. 8-9)
+              float2 b1[PPT / 2], b2[PPT / 2];
+#pragma unroll
+              for (int hq = 0; hq < PPT / 2; ++hq) {
+                b1[hq] = make_float2(0.f, 0.f);
+                b2[hq] = make_float2(0.f, 0.f);
+              }
+              auto step = [&](float a) {
+#pragma unroll
+                for (int hq = 0; hq < PPT / 2; ++hq) {
+                  const float2 t = __ffma2_rn(b2[hq], neg1, make_float2(a, a));   // a - b_{k+2}
+                  const float2 n = __ffma2_rn(c2[hq], b1[hq], t);
+                  b2[hq] = b1[hq];
+                  b1[hq] = n;
+                }
+              };
+              float4 tc = rowq[0];
+#pragma unroll 2
+              for (int i4 = 0; i4 < n4 - 1; ++i4) {
+                const float4 tn = rowq[i4 + 1];
+                step(tc.x);
+                step(tc.y);
+                step(tc.z);
+                step(tc.w);
+                tc = tn;
+              }
+              step(tc.x);
+              step(tc.y);
+              step(tc.z);                                           // -> b_1, b_2
+#pragma unroll
+              for (int q = 0; q < PPT; ++q) {
+                const float bb1 = (q & 1) ? b1[q >> 1].y : b1[q >> 1].x;
+                const float bb2 = (q & 1) ? b2[q >> 1].y : b2[q >> 1].x;
+                const float accr = fmaf(cf[q], bb1, tc.w - bb2);     // a'_0 + z b_1 - b_2
+                const float acci = sf[q] * bb1;
+                const float mr = nrf[q] * accr - nif[q] * acci;      // mu_s = I_0 sum
+                const float mi = nrf[q] * acci + nif[q] * accr;
+                yr[q] += (double)fmaf(mr, prr[q], -mi * pri[q]);     // Y += gamma mu e^{i theta_s}
+                yi[q] += (double)fmaf(mr, pri[q], mi * prr[q]);
+                const float npr = fmaf(prr[q], drr[q], -pri[q] * dri[q]);
+                pri[q] = fmaf(prr[q], dri[q], pri[q] * drr[q]);
+                prr[q] = npr;
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < PPT; ++q) {
+              const double t2 = fma(xs[q], (double)(Ks * G), th[q]);
               th[q] = t2 - 2.0 * rint(0.5 * t2);
             }
             continue;
@@ -777,7 +793,7 @@ int launch_integrand(const KParams& p, const int* list, long long n_list, bool c
 __global__ void __launch_bounds__(BLOCK) reduce_kernel(const RParams p) {
   __shared__ double red[6][BLOCK];
   const int ci = blockIdx.x;
-  const long long r0 = p.coi_off[ci], r1 = p.coi_off[ci + 1];
+  const long long r0 = max(p.coi_off[ci], p.r_lo), r1 = min(p.coi_off[ci + 1], p.r_hi);
   double acc[6] = {0, 0, 0, 0, 0, 0};
   for (long long r = r0 + threadIdx.x; r < r1; r += BLOCK) {
     const RegionDesc rd = p.desc[r];
@@ -801,6 +817,10 @@ __global__ void __launch_bounds__(BLOCK) reduce_kernel(const RParams p) {
       for (int k = 0; k < 6; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + s];
     __syncthreads();
   }
+  if (threadIdx.x == 0 && p.part_out) {          // shard mode: raw sums, combined later
+    for (int k = 0; k < 6; ++k) p.part_out[(size_t)ci * 6 + k] = red[k][0];
+    return;
+  }
   if (threadIdx.x == 0) {
     const int kappa = p.coi[ci];
     const double Pk = p.P[kappa];
@@ -815,6 +835,33 @@ __global__ void __launch_bounds__(BLOCK) reduce_kernel(const RParams p) {
     p.eta[ci] = e;
     p.npts[ci] = red[5][0];
   }
+}
+
+// Multi-GPU combine: the per-COI sums of every shard, added in fixed rank order
+// (bitwise identical on every rank), then the Eq. 11 scale.
+__global__ void combine_kernel(const CParams p) {
+  const int ci = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ci >= p.n_coi) return;
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  for (int r = 0; r < p.world; ++r)
+    for (int k = 0; k < 6; ++k) acc[k] += p.gathered[((size_t)r * p.n_coi + ci) * 6 + k];
+  const int kappa = p.coi[ci];
+  const double Pk = p.P[kappa];
+  const double scale = p.R[kappa] / (Pk * Pk * Pk) * p.inv_fs;
+  double e = 0.0;
+  for (int k = 0; k < 5; ++k) {
+    const double t = acc[k] * scale;
+    if (p.terms) p.terms[(size_t)ci * 5 + k] = t;
+    e += t;
+  }
+  p.eta[ci] = e;
+  if (p.npts) p.npts[ci] = acc[5];
+}
+
+int launch_combine(const CParams& p, void* stream) {
+  if (p.n_coi <= 0) return 0;
+  combine_kernel<<<(p.n_coi + 127) / 128, 128, 0, (cudaStream_t)stream>>>(p);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 int launch_reduce(const RParams& p, void* stream) {

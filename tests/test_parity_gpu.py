@@ -211,6 +211,30 @@ def test_unit_link_3d_through_cuda(isrs):
     assert abs(e_g[0] - egn.unit_link_eta_3d(-1.0, 4.0)) < 2e-3
 
 
+@pytest.mark.parametrize("cfg,coi,world", [("c1", None, 3), ("c2", None, 2), ("c2", [0, 19, 39], 4),
+                                            ("c4", [7, 41], 3)])
+def test_shards_combine_to_the_single_gpu_eta(isrs, cfg, coi, world):
+    """shard r of `world` + all-gather + combine == the one-GPU eta (<= 1e-12; only the
+    summation order differs), bitwise reproducible, and the shards' work adds up."""
+    link = bj_config(cfg)
+    with isrs.Engine(link) as e:
+        full, tfull = e.nli(coi=coi, terms=True)
+        pts_full = e.work()[0]
+        sums, pts = [], 0
+        for r in range(world):
+            sums.append(e.nli_shard(r, world, coi=coi))
+            pts += e.work()[0]
+        g = torch.stack(sums)
+        eta, terms = e.combine(g, coi=coi, terms=True)
+        eta2 = e.combine(g.clone(), coi=coi)
+        torch.cuda.synchronize()
+        full, eta, eta2 = full.cpu().numpy(), eta.cpu().numpy(), eta2.cpu().numpy()
+    assert pts == pts_full
+    assert np.all(np.abs(eta - full) / full <= 1e-12), np.abs(eta - full) / full
+    assert np.array_equal(eta, eta2)
+    assert np.allclose(terms.cpu().numpy(), tfull.cpu().numpy(), rtol=1e-12, atol=1e-12 * np.abs(full).max())
+
+
 DB_TOL_FP32 = 1e-3     # north star: optional fp32 path within 0.001 dB
 
 

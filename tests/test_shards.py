@@ -1,0 +1,97 @@
+"""Multi-GPU sharding host logic — runs on CPU.
+
+isrs_egn_plan_shards is the host planner every rank runs before its isrs_egn_nli_shard call; it
+touches no device.  Checked here: shards are contiguous, disjoint, cover the canonical region list,
+conserve the in-support point count, and balance cost; and across a real 2-process gloo group each
+rank's own plan agrees with the others' (what the ranks all-gather must tile the whole work list).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from workloads import bj_config, tiny_link  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def isrs():
+    from paper_2412_11614_b200 import build
+    build.build()
+    import paper_2412_11614_b200 as m
+    return m
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3"])
+def test_shards_tile_the_work_list(isrs, cfg):
+    link = bj_config(cfg)
+    r1, p1, f1 = isrs.plan_shards(link, 1)
+    assert f1[0] == 0
+    for world in (2, 3, 4, 8):
+        r, p, f = isrs.plan_shards(link, world)
+        assert r.sum() == r1[0] and p.sum() == p1[0]
+        assert np.all(f[1:] == f[:-1] + r[:-1])          # contiguous, in rank order
+        if world <= r1[0] // 4:
+            assert p.max() / p.mean() < 1.05, (cfg, world, p)
+
+
+def test_shards_with_coi_subset_and_3d(isrs):
+    link = tiny_link(n_ch=5, rates_gbd=(32, 64, 96), guard_ghz=12.5, n_span=2, grid_n=8)
+    full = isrs.plan_shards(link, 1, coi=[4, 0, 2])
+    r, p, _ = isrs.plan_shards(link, 3, coi=[4, 0, 2])
+    assert r.sum() == full[0][0] and p.sum() == full[1][0]
+    r3, p3, _ = isrs.plan_shards(link, 1, coi=[4, 0, 2], f_samples=4)
+    assert r3[0] == 4 * full[0][0] or r3[0] > full[0][0]   # every f sample lists its own regions
+
+
+def test_plan_rejects_bad_world(isrs):
+    with pytest.raises(isrs.IsrsEgnError):
+        isrs.plan_shards(bj_config("c1"), 0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, cfg, q):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+    import paper_2412_11614_b200 as m
+    from workloads import bj_config as bj
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    link = bj(cfg)
+    r, p, f = m.plan_shards(link, world)
+    mine = torch.tensor([r[rank], p[rank], f[rank]], dtype=torch.int64)
+    got = [torch.zeros(3, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(got, mine)
+    got = torch.stack(got).numpy()
+    full = m.plan_shards(link, 1)
+    ok = (got[:, 0].sum() == full[0][0] and got[:, 1].sum() == full[1][0] and got[0, 2] == 0
+          and all(got[i + 1, 2] == got[i, 2] + got[i, 0] for i in range(world - 1)))
+    dist.barrier()
+    dist.destroy_process_group()
+    q.put((rank, bool(ok), got.tolist()))
+
+
+def test_gloo_two_ranks_agree_on_the_shard_plan():
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, "c2", q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _ in res), res
+    assert res[0][2] == res[1][2]
