@@ -68,9 +68,19 @@ enum { ISRS_EGN_MU_SEGMENT = 0,    /* Eqs. 8-10 (default, the hot path)         
        ISRS_EGN_MU_MACLAURIN = 1   /* Eq. 4 (NEXT-1)                                          */ };
 
 enum { ISRS_EGN_FLAG_UNIT_LINK = 1u, /* test hook: Y := 1 (oracle pin P6)                    */
-       ISRS_EGN_FLAG_NO_CHAIN = 2u   /* evaluate every span's segment sum (Eq. 8) on its own
+       ISRS_EGN_FLAG_NO_CHAIN = 2u,  /* evaluate every span's segment sum (Eq. 8) on its own
                                         instead of chaining runs of identical consecutive spans
-                                        into one recurrence (R9); same sum, A/B hook */ };
+                                        into one recurrence (R9); same sum, A/B hook */
+       ISRS_EGN_FLAG_DEDUP = 4u,     /* span-class dedup (SURVEY §8(f) NEXT-4a): for G identical
+                                        consecutive spans evaluate the K-segment sum ONCE per point
+                                        and multiply by the phased-array factor sum_g e^{i g chi L};
+                                        same Y (Eq. 22), ~G x less work.  Its rate is reported
+                                        separately, never as the headline point-spans/s */
+       ISRS_EGN_FLAG_LITERAL_GAIN = 8u /* NEXT-4b (R11): Eq. 22's gain / sqrt(rho) products
+                                        as printed with a transparent scalar gain g_s = e^{alpha_s L_s}
+                                        (mean loss restored, SRS tilt persists) instead of reading C3's
+                                        ideal per-frequency equalisation (products = 1); fp64 segment
+                                        mode only */ };
 
 typedef struct {
   int32_t grid_n;      /* N: N x N bin-centre grid per (kappa1, kappa2) region; even, >= 2 (C6) */

@@ -112,7 +112,7 @@ def island_gates(c: Canon, f3: np.ndarray):
 
 
 def region_islands(c: Canon, kappa: int, k1: int, k2: int, mu_mode: str = "closed",
-                   need=("D", "E", "F", "G", "H"), f=None):
+                   need=("D", "E", "F", "G", "H"), f=None, gain: str = "ideal"):
     """Per-island raw integrals D, E, F, G, H of region (kappa, k1, k2) (Eqs. 17-21, C6, C7, C10)
     at NLI frequency f (default: the COI centre)."""
     f = c.f[kappa] if f is None else f
@@ -128,7 +128,7 @@ def region_islands(c: Canon, kappa: int, k1: int, k2: int, mu_mode: str = "close
         Y[support] = 1.0
     else:
         Y[support] = link_mod.link_function(F1[support], F2[support], f, c.spans,
-                                            c.p_tot, c.b_tot, c.dz, mu_mode)
+                                            c.p_tot, c.b_tot, c.dz, mu_mode, gain)
     d1, d2 = c.delta[k1], c.delta[k2]
     N = c.N
     m1 = np.arange(N)[None, :] * np.ones((N, 1), dtype=np.int64)
@@ -199,7 +199,8 @@ def island_contributions(c: Canon, k1: int, k2: int, isl: dict):
     return np.array([tD, tE, tF, tG, tH])
 
 
-def eta(link, coi=None, mu_mode: str = "closed", return_regions: bool = False, f_samples: int = 0):
+def eta(link, coi=None, mu_mode: str = "closed", return_regions: bool = False, f_samples: int = 0,
+        gain: str = "ideal"):
     """eta_kappa (1/W^2, Eq. 11 with P = P_kappa, reading C13) and the D/E/F/G/H breakdown.
 
     Brute force over every (kappa1, kappa2) pair and every grid point (Eq. 16 generalised to
@@ -220,7 +221,7 @@ def eta(link, coi=None, mu_mode: str = "closed", return_regions: bool = False, f
                 for k2 in range(n):
                     if not has_support_bound(c, kappa, k1, k2, f):
                         continue
-                    isls = region_islands(c, kappa, k1, k2, mu_mode, _needed_terms(c, k1, k2), f)
+                    isls = region_islands(c, kappa, k1, k2, mu_mode, _needed_terms(c, k1, k2), f, gain)
                     if not isls:
                         continue
                     if return_regions:

@@ -16,6 +16,8 @@ OK, EINVAL, EOVERLAP, ERANGE, ENOMEM, ECUDA, EUNSUPPORTED = 0, -1, -2, -3, -4, -
 MU_SEGMENT, MU_MACLAURIN = 0, 1
 FLAG_UNIT_LINK = 1
 FLAG_NO_CHAIN = 2
+FLAG_DEDUP = 4
+FLAG_LITERAL_GAIN = 8
 
 EXPORTED = ("isrs_egn_create", "isrs_egn_nli", "isrs_egn_region_partials", "isrs_egn_work",
             "isrs_egn_eta_host", "isrs_egn_last_kernel_ms", "isrs_egn_last_launch_count",

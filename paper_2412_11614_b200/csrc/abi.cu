@@ -82,6 +82,7 @@ struct isrs_egn {
   DevBuf<long long> d_rate;
   DevBuf<double> d_A2, d_A3, d_Eh, d_ah, d_gh, d_macc, d_aL;
   DevBuf<int> d_K, d_cls, d_Kc, d_chain_s0, d_chain_g;
+  DevBuf<double> d_lnc_L, d_zeta_L, d_lgA, d_lgB, d_lgC, d_lgD;
   int n_chain = 0;
   std::vector<int> chain_g, k_s;
   DevBuf<double> d_lnA, d_zeta;
@@ -128,6 +129,9 @@ static int validate(const isrs_egn_problem* p, const isrs_egn_numerics* n) {
     return fail(ISRS_EGN_EUNSUPPORTED, "precision must be 64 or 32");
   if (n->precision == 32 && n->mu_mode != ISRS_EGN_MU_SEGMENT)
     return fail(ISRS_EGN_EUNSUPPORTED, "precision 32 (row a8) is a variant of the segment mode only");
+  if ((n->flags & ISRS_EGN_FLAG_LITERAL_GAIN) &&
+      (n->mu_mode != ISRS_EGN_MU_SEGMENT || n->precision == 32 || (n->flags & ISRS_EGN_FLAG_DEDUP)))
+    return fail(ISRS_EGN_EUNSUPPORTED, "LITERAL_GAIN is an fp64 segment-mode variant (no DEDUP)");
   if (n->f_samples < 0 || n->f_samples > 4096) return fail(ISRS_EGN_EINVAL, "f_samples must be in [0, 4096]");
   if (n->mu_mode != ISRS_EGN_MU_SEGMENT && n->mu_mode != ISRS_EGN_MU_MACLAURIN)
     return fail(ISRS_EGN_EUNSUPPORTED, "unknown mu_mode");
@@ -270,7 +274,8 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
   // (common subexpressions), but every span keeps its own K-segment recurrence; cap 1024 spans
   const bool chain_ok = num.mu_mode == ISRS_EGN_MU_SEGMENT &&
                         !(num.flags & (ISRS_EGN_FLAG_NO_CHAIN | ISRS_EGN_FLAG_UNIT_LINK));
-  const long long chain_cap = (num.precision == 32) ? 1024LL * 1000000 : CHAIN_MAX;
+  const bool dedup = (num.flags & ISRS_EGN_FLAG_DEDUP) && num.precision == 64;
+  const long long chain_cap = (num.precision == 32 || dedup) ? 1024LL * 1000000 : CHAIN_MAX;
   for (int s = 0; s < p->n_span; ++s) {
     const bool same = s > 0 && chain_ok && (num.precision == 32 || K[s] % 2 == 0) &&
                       p->length_m[s] == p->length_m[s - 1] &&
@@ -279,7 +284,7 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
                       p->beta3_s3_per_m[s] == p->beta3_s3_per_m[s - 1] &&
                       p->gamma_per_w_m[s] == p->gamma_per_w_m[s - 1] &&
                       p->cr_per_w_m_hz[s] == p->cr_per_w_m_hz[s - 1] &&
-                      (long long)(ch_g.back() + 1) * (num.precision == 32 ? 1000000 : K[s]) <= chain_cap;
+                      (long long)(ch_g.back() + 1) * ((num.precision == 32 || dedup) ? 1000000 : K[s]) <= chain_cap;
     if (same) {
       ch_g.back() += 1;
     } else {
@@ -288,6 +293,23 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
     }
   }
   h->n_chain = (int)ch_s0.size();
+  // ---- literal gain products (NEXT-4b): SRS gain at each span end, prefix / suffix sums
+  const int ns = p->n_span;
+  std::vector<double> lncL(ns), zL(ns), lgA(ns, 0.0), lgB(ns, 0.0), lgC(ns, 0.0), lgD(ns, 0.0);
+  for (int s = 0; s < ns; ++s) {
+    const double a = p->alpha_per_m[s], L = p->length_m[s];
+    zL[s] = h->p_tot * p->cr_per_w_m_hz[s] * (-std::expm1(-a * L) / a);   // Eq. 2 at z = L
+    const double x = h->b_tot * zL[s];
+    lncL[s] = (x == 0.0) ? 0.0 : std::log(x / (2.0 * std::sinh(0.5 * x)));   // Eq. 14
+  }
+  for (int s = 1; s < ns; ++s) {
+    lgA[s] = lgA[s - 1] + 3.0 * lncL[s - 1];
+    lgB[s] = lgB[s - 1] + zL[s - 1];
+  }
+  for (int s = ns - 2; s >= 0; --s) {
+    lgC[s] = lgC[s + 1] + lncL[s + 1];
+    lgD[s] = lgD[s + 1] + zL[s + 1];
+  }
   h->chain_g = ch_g;
   h->k_s = K;
   int kmax = *std::max_element(cK.begin(), cK.end());
@@ -311,7 +333,9 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
             h->d_rate.upload(h->rate) && h->d_A2.upload(A2) && h->d_A3.upload(A3) &&
             h->d_Eh.upload(Eh) && h->d_ah.upload(ah) && h->d_gh.upload(gh) &&
             h->d_macc.upload(macc) && h->d_aL.upload(aL) && h->d_K.upload(K) && h->d_cls.upload(cls) &&
-            h->d_Kc.upload(cK) && h->d_chain_s0.upload(ch_s0) && h->d_chain_g.upload(ch_g);
+            h->d_Kc.upload(cK) && h->d_chain_s0.upload(ch_s0) && h->d_chain_g.upload(ch_g) &&
+            h->d_lnc_L.upload(lncL) && h->d_zeta_L.upload(zL) && h->d_lgA.upload(lgA) &&
+            h->d_lgB.upload(lgB) && h->d_lgC.upload(lgC) && h->d_lgD.upload(lgD);
   DevBuf<double> dL, dA, dC;
   ok = ok && dL.upload(cL) && dA.upload(cA) && dC.upload(cC) &&
        h->d_lnA.alloc((size_t)h->n_cls * h->kstride) && h->d_zeta.alloc((size_t)h->n_cls * h->kstride);
@@ -518,12 +542,16 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
   kp.mac_c = h->d_macc.p; kp.aL = h->d_aL.p; kp.K = h->d_K.p; kp.cls = h->d_cls.p;
   kp.n_span = h->n_span;
   kp.chain_s0 = h->d_chain_s0.p; kp.chain_g = h->d_chain_g.p; kp.n_chain = h->n_chain;
+  kp.lnc_L = h->d_lnc_L.p; kp.zeta_L = h->d_zeta_L.p; kp.lgA = h->d_lgA.p; kp.lgB = h->d_lgB.p;
+  kp.lgC = h->d_lgC.p; kp.lgD = h->d_lgD.p;
   kp.lnA = h->d_lnA.p; kp.zeta = h->d_zeta.p; kp.Kc = h->d_Kc.p; kp.n_cls = h->n_cls;
   kp.kstride = h->kstride; kp.tstride = h->tstride; kp.tw = h->tw; kp.N = h->N;
   kp.fv = h->d_fv.p; kp.desc = h->d_desc.p; kp.partials = h->d_partials.p;
   kp.mode = (h->num.flags & ISRS_EGN_FLAG_UNIT_LINK) ? MODE_UNIT
             : (h->num.mu_mode == ISRS_EGN_MU_MACLAURIN ? MODE_MACLAURIN
-               : (h->num.precision == 32 ? MODE_SEG32 : MODE_SEGMENT));
+               : (h->num.precision == 32 ? MODE_SEG32
+                  : ((h->num.flags & ISRS_EGN_FLAG_DEDUP) ? MODE_SEGDD
+                     : ((h->num.flags & ISRS_EGN_FLAG_LITERAL_GAIN) ? MODE_SEGLG : MODE_SEGMENT))));
   if (!h->ev[0]) {
     for (auto& e : h->ev)
       if (cudaEventCreate(&e) != cudaSuccess) return cuda_fail(cudaGetLastError(), "cudaEventCreate");

@@ -43,7 +43,10 @@ enum : int { NEED_E = 1, NEED_F = 2, NEED_G = 4, NEED_H = 8, FV_SHIFT = 8 };
 
 // MODE_SEG32: row a8, the mixed fp32 variant of the segment form (fp32 recurrence, mu, phase
 // factor; fp64 chi h and its exact reduction, the phase advance and every accumulation)
-enum : int { MODE_SEGMENT = 0, MODE_MACLAURIN = 1, MODE_UNIT = 2, MODE_SEG32 = 3 };
+// MODE_SEGDD: the segment form with span-class dedup (NEXT-4a, ISRS_EGN_FLAG_DEDUP)
+// MODE_SEGLG: the segment form with the literal gain products of Eq. 22 (NEXT-4b)
+enum : int { MODE_SEGMENT = 0, MODE_MACLAURIN = 1, MODE_UNIT = 2, MODE_SEG32 = 3, MODE_SEGDD = 4,
+             MODE_SEGLG = 5 };
 
 struct RegionDesc {
   int kappa, k1, k2, flags;
@@ -79,6 +82,14 @@ struct KParams {
   const int* chain_s0;
   const int* chain_g;
   int n_chain;
+  // literal gain (NEXT-4b): ln S_s(x) = lnc_L[s] - zeta_L[s] x is the SRS gain at the end of span s;
+  // ln Lambda_s = (lgA - lgB (f1+f2+f3)) / 2 + (lgC - lgD f) / 2 with prefix (A, B) / suffix (C, D) sums
+  const double* lnc_L;
+  const double* zeta_L;
+  const double* lgA;
+  const double* lgB;
+  const double* lgC;
+  const double* lgD;
   // span classes: envelope a'_k(f3) = exp(lnA[c][k] - zeta[c][k] f3)
   const double* lnA;    // [n_cls][kstride]  ln(c_k) - alpha h k
   const double* zeta;   // [n_cls][kstride]

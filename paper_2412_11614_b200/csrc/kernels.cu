@@ -283,6 +283,9 @@ template <bool COH, int MODE>
 __global__ void __launch_bounds__(BLOCK, MIN_BLOCKS)
 integrand_kernel(const KParams p, const int* __restrict__ list) {
   extern __shared__ __align__(16) char smem_raw[];
+  constexpr bool SEGM = (MODE == MODE_SEGMENT || MODE == MODE_SEGDD || MODE == MODE_SEGLG);
+  constexpr bool LG = (MODE == MODE_SEGLG);   // literal Eq. 22 gain products (NEXT-4b)
+  constexpr bool DEDUP = (MODE == MODE_SEGDD);
   Smem sm;
   smem_layout(p.tstride, p.tw, p.N, COH, smem_raw, &sm);
   const int tid = threadIdx.x;
@@ -435,7 +438,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
           // chain of G identical consecutive spans starting at s (G = 1 unless chained, R9)
           const int s = __ldg(p.chain_s0 + ch), G = __ldg(p.chain_g + ch);
           const int cls = __ldg(p.cls + s);
-          if ((MODE == MODE_SEGMENT || MODE == MODE_SEG32) &&
+          if ((SEGM || MODE == MODE_SEG32) &&
               (cls != tcls || i_first < tb || i_last >= tb + tn)) {
             // ---- (re)build the envelope table rows for compacted lines [tb, tb + tn)
             __syncthreads();
@@ -570,7 +573,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
             sincospi_d(x[q], &sn[q], &cs[q]);        // z = e^{i chi h}
           }
           double accr[PPT], acci[PPT];
-          if (MODE == MODE_SEGMENT) {
+          if (SEGM) {
             // ---- Goertzel over the K_s segments (Eqs. 8-9 with I_k = I_0 w^k)
             const int Kp = (__ldg(p.Kc + cls) + 1) & ~1;
             double c2[PPT], b1[PPT], b2[PPT];
@@ -587,8 +590,20 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
             // span chain (R9): the coefficients of G identical spans repeat with period K, so
             // the row is walked G times (rowp[npair] holds a copy of rowp[0] for the wrap)
             double2 tc = rowp[0];
-            for (int gi = 0; gi < G; ++gi) {
-              const int nit = (gi == G - 1) ? npair - 1 : npair;
+            const int Gr = DEDUP ? 1 : G;        // NEXT-4a: one span's sum, reused below
+            // NEXT-4b: span g of the chain carries Lambda_{s+g} = Lambda_s r^g with r = S_L(f3), the
+            // SRS gain at the span end (identical spans); blocks run from g = G-1 down, so the
+            // recurrence state is scaled by r at every block boundary (linear in the coefficients)
+            const double rlg = LG ? exp(__ldg(p.lnc_L + s) - __ldg(p.zeta_L + s) * f3l) : 1.0;
+            for (int gi = 0; gi < Gr; ++gi) {
+              const int nit = (gi == Gr - 1) ? npair - 1 : npair;
+              if (LG && gi > 0) {
+#pragma unroll
+                for (int q = 0; q < PPT; ++q) {
+                  b1[q] *= rlg;
+                  b2[q] *= rlg;
+                }
+              }
               ISRS_UNROLL_PRAGMA(ISRS_UNROLL)
               for (int i2 = 0; i2 < nit; ++i2) {
                 const double2 tn = rowp[i2 + 1];
@@ -611,12 +626,29 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
               accr[q] = fma(cs[q], n0, tc.y - b1[q]);
               acci[q] = sn[q] * n0;
             }
+            if (DEDUP && G > 1) {
+              // NEXT-4a: x sum_{g<G} rho^g, rho = e^{i chi L} (the identical spans' phases, C3)
+#pragma unroll
+              for (int q = 0; q < PPT; ++q) {
+                double rs, rc;
+                sincospi_d(x[q] * Ks, &rs, &rc);
+                double gr = 1.0, gim = 0.0;
+                for (int g2 = 1; g2 < G; ++g2) {
+                  const double t = fma(gr, rc, fma(-gim, rs, 1.0));
+                  gim = fma(gr, rs, gim * rc);
+                  gr = t;
+                }
+                const double ar = accr[q];
+                accr[q] = fma(ar, gr, -acci[q] * gim);
+                acci[q] = fma(ar, gim, acci[q] * gr);
+              }
+            }
           }
 #pragma unroll
           for (int q = 0; q < PPT; ++q) {
             const double px = CUDART_PI * x[q];     // chi h
             double mr, mi;
-            if (MODE == MODE_SEGMENT) {
+            if (SEGM) {
               // I_0 = (w - 1)/(i chi - alpha) = h (w - 1) conj(d) / |d|^2, d = -alpha h + i chi h
               const double wr1 = fma(Eh, cs[q], -1.0), wi = Eh * sn[q];
               const double inv = gh * rcp_d(fma(px, px, ah * ah));   // gamma_s h / |d|^2
@@ -646,6 +678,12 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
               // (values above are eta / h; gh = gamma h restores the scale)
               mr = (eta_r - cf * (eta_r - et2_r)) * gh;
               mi = (eta_i - cf * (eta_i - et2_i)) * gh;
+            }
+            if (LG) {   // Lambda_s of the chain's first span (prefix / suffix sums)
+              const double lam = exp(0.5 * (fma(-__ldg(p.lgB + s), 2.0 * f3l + f, __ldg(p.lgA + s)) +
+                                            fma(-__ldg(p.lgD + s), f, __ldg(p.lgC + s))));
+              mr *= lam;
+              mi *= lam;
             }
             // Y += gamma_s mu_s e^{i theta_s}, theta_s = pi * th (reading C3)
             double ps = 0.0, pc = 1.0;                  // theta_1 = 0 for the first chain
@@ -778,11 +816,15 @@ int launch_integrand(const KParams& p, const int* list, long long n_list, bool c
   if (coherent) {
     if (p.mode == MODE_SEGMENT) return launch_one<true, MODE_SEGMENT>(p, list, n_list, st);
     if (p.mode == MODE_SEG32) return launch_one<true, MODE_SEG32>(p, list, n_list, st);
+    if (p.mode == MODE_SEGDD) return launch_one<true, MODE_SEGDD>(p, list, n_list, st);
+    if (p.mode == MODE_SEGLG) return launch_one<true, MODE_SEGLG>(p, list, n_list, st);
     if (p.mode == MODE_MACLAURIN) return launch_one<true, MODE_MACLAURIN>(p, list, n_list, st);
     return launch_one<true, MODE_UNIT>(p, list, n_list, st);
   }
   if (p.mode == MODE_SEGMENT) return launch_one<false, MODE_SEGMENT>(p, list, n_list, st);
   if (p.mode == MODE_SEG32) return launch_one<false, MODE_SEG32>(p, list, n_list, st);
+  if (p.mode == MODE_SEGDD) return launch_one<false, MODE_SEGDD>(p, list, n_list, st);
+  if (p.mode == MODE_SEGLG) return launch_one<false, MODE_SEGLG>(p, list, n_list, st);
   if (p.mode == MODE_MACLAURIN) return launch_one<false, MODE_MACLAURIN>(p, list, n_list, st);
   return launch_one<false, MODE_UNIT>(p, list, n_list, st);
 }
@@ -828,9 +870,9 @@ __global__ void __launch_bounds__(BLOCK) reduce_kernel(const RParams p) {
     const double scale = p.R[kappa] / (Pk * Pk * Pk) * p.inv_fs;
     double e = 0.0;
     for (int k = 0; k < 5; ++k) {
-      const double t = red[k][0] * scale;
+      const double t = __dmul_rn(red[k][0], scale);   // no contraction: eta independent of terms
       if (p.terms) p.terms[(size_t)ci * 5 + k] = t;
-      e += t;
+      e = __dadd_rn(e, t);
     }
     p.eta[ci] = e;
     p.npts[ci] = red[5][0];
@@ -850,9 +892,9 @@ __global__ void combine_kernel(const CParams p) {
   const double scale = p.R[kappa] / (Pk * Pk * Pk) * p.inv_fs;
   double e = 0.0;
   for (int k = 0; k < 5; ++k) {
-    const double t = acc[k] * scale;
+    const double t = __dmul_rn(acc[k], scale);   // no contraction: eta independent of terms
     if (p.terms) p.terms[(size_t)ci * 5 + k] = t;
-    e += t;
+    e = __dadd_rn(e, t);
   }
   p.eta[ci] = e;
   if (p.npts) p.npts[ci] = acc[5];

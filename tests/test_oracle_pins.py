@@ -337,6 +337,46 @@ def test_P14_unit_link_3d_closed_form(fmt):
     assert 3.5 < errs[0] / errs[1] < 4.5 and 3.5 < errs[1] / errs[2] < 4.5, errs
 
 
+# ---------------------------------------------------------------- NEXT-4b literal gain (R11)
+
+def _pts(c, kappa=1, k1=0, k2=2, n=6):
+    F1, F2, f3 = egn.region_points(c, kappa, k1, k2)
+    return F1.ravel()[:n * 7:7], F2.ravel()[:n * 7:7], c.f[kappa]
+
+
+def test_P15_literal_gain_reduces_to_ideal_at_cr0_and_one_span():
+    # Eq. 22 as printed with g = e^{alpha L}: at C_r = 0, g rho = 1 (Eq. 25), so every product is 1;
+    # with one span both products are empty.
+    l0 = tiny_link(n_ch=3, rates_gbd=(64,), n_span=3, grid_n=8, cr_w_km_thz=0.0, random_spans=True)
+    c0 = egn.canonicalize(l0)
+    f1, f2, f = _pts(c0)
+    a = link_mod.link_function(f1, f2, f, c0.spans, c0.p_tot, c0.b_tot, c0.dz, "closed", "literal")
+    b = link_mod.link_function(f1, f2, f, c0.spans, c0.p_tot, c0.b_tot, c0.dz, "closed", "ideal")
+    assert _rel(a, b) < 1e-13
+    l1 = tiny_link(n_ch=3, rates_gbd=(64,), n_span=1, grid_n=8, cr_w_km_thz=1.0, power_dbm=10.0)
+    c1 = egn.canonicalize(l1)
+    f1, f2, f = _pts(c1)
+    a = link_mod.link_function(f1, f2, f, c1.spans, c1.p_tot, c1.b_tot, c1.dz, "closed", "literal")
+    b = link_mod.link_function(f1, f2, f, c1.spans, c1.p_tot, c1.b_tot, c1.dz, "closed", "ideal")
+    assert np.array_equal(a, b)
+
+
+def test_P15_literal_gain_span_ratio_is_the_srs_gain_at_f3():
+    # identical spans: Lambda_{s+1} / Lambda_s = g^{3/2} sqrt(rho(f1) rho(f3) rho(f2)) / (g^{1/2} sqrt(rho(f)))
+    # = c e^{-zeta (f1 + f2 + f3 - f) / 2} = c e^{-zeta f3} (f1 + f2 = f3 + f): the SRS gain at the
+    # end of a span, Eq. 14 at z = L and frequency f1 + f2 - f.  Evaluated here from Eq. 14 directly.
+    l = tiny_link(n_ch=3, rates_gbd=(96,), n_span=3, grid_n=8, cr_w_km_thz=1.0, power_dbm=12.0)
+    c = egn.canonicalize(l)
+    f1, f2, f = _pts(c)
+    lam = link_mod._gain_products(f1, f2, f, c.spans, c.p_tot, c.b_tot)
+    sp = c.spans[0]
+    zeta = c.p_tot * sp["cr"] * (1.0 - math.exp(-sp["alpha"] * sp["L"])) / sp["alpha"]
+    x = c.b_tot * zeta
+    want = x / (2.0 * math.sinh(x / 2.0)) * np.exp(-zeta * (f1 + f2 - f))
+    assert _rel(lam[1] / lam[0], want) < 1e-12 and _rel(lam[2] / lam[1], want) < 1e-12
+    assert np.any(np.abs(want - 1.0) > 1e-3)      # the tilt is not negligible here
+
+
 def test_P10_grid_convergence_order_two():
     # single 10 GBd channel, 1 span: successive differences fall ~4x per halving of delta (midpoint rule)
     vals = []

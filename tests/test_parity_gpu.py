@@ -235,6 +235,44 @@ def test_shards_combine_to_the_single_gpu_eta(isrs, cfg, coi, world):
     assert np.allclose(terms.cpu().numpy(), tfull.cpu().numpy(), rtol=1e-12, atol=1e-12 * np.abs(full).max())
 
 
+@pytest.mark.parametrize("name", ["long_link_chained", "uniform_64gbd_2span", "random_spans_multiclass"])
+def test_dedup_mode_parity_tiny(isrs, name):
+    """NEXT-4a: span-class dedup (one K-segment sum x the phased-array factor) is the same Y."""
+    link = tiny_link(**TINY[name])
+    e_o, _ = egn.eta(link)
+    e_g, _ = gpu_eta(isrs, link, flags=isrs.FLAG_DEDUP)
+    assert np.all(np.abs(e_g - e_o) / e_o <= TOL_ETA), (name, np.abs(e_g - e_o) / e_o)
+
+
+@pytest.mark.parametrize("cfg,coi", [("c2", None), ("c5", [100])])
+def test_dedup_mode_matches_full_evaluation(isrs, cfg, coi):
+    link = bj_config(cfg)
+    a, _ = gpu_eta(isrs, link, coi=coi, flags=isrs.FLAG_DEDUP)
+    b, _ = gpu_eta(isrs, link, coi=coi)
+    assert np.all(np.abs(a - b) / b <= TOL_ETA), np.abs(a - b) / b
+
+
+@pytest.mark.parametrize("name", ["long_link_chained", "random_spans_multiclass", "strong_isrs",
+                                  "mixed_rates_guard"])
+def test_literal_gain_parity_tiny(isrs, name):
+    """NEXT-4b: Eq. 22's gain / sqrt(rho) products as printed (R11), against the oracle written
+    literally from the products."""
+    link = tiny_link(**TINY[name])
+    e_o, t_o = egn.eta(link, gain="literal")
+    e_g, t_g = gpu_eta(isrs, link, flags=isrs.FLAG_LITERAL_GAIN)
+    assert np.all(np.abs(e_g - e_o) / e_o <= TOL_ETA), (name, np.abs(e_g - e_o) / e_o)
+    e_i, _ = egn.eta(link)
+    if name in ("strong_isrs", "long_link_chained"):
+        assert np.max(np.abs(e_o - e_i) / e_i) > 1e-4      # the persistent tilt is visible
+
+
+def test_literal_gain_chained_matches_unchained_c2(isrs):
+    link = bj_config("c2")
+    a, _ = gpu_eta(isrs, link, coi=[0, 19, 39], flags=isrs.FLAG_LITERAL_GAIN)
+    b, _ = gpu_eta(isrs, link, coi=[0, 19, 39], flags=isrs.FLAG_LITERAL_GAIN | isrs.FLAG_NO_CHAIN)
+    assert np.all(np.abs(a - b) / b <= TOL_ETA), np.abs(a - b) / b
+
+
 DB_TOL_FP32 = 1e-3     # north star: optional fp32 path within 0.001 dB
 
 
