@@ -65,7 +65,10 @@ typedef struct {
 } isrs_egn_problem;
 
 enum { ISRS_EGN_MU_SEGMENT = 0,    /* Eqs. 8-10 (default, the hot path)                       */
-       ISRS_EGN_MU_MACLAURIN = 1   /* Eq. 4 (NEXT-1)                                          */ };
+       ISRS_EGN_MU_MACLAURIN = 1,  /* Eq. 4 (NEXT-1)                                          */
+       ISRS_EGN_MU_INTEGRAL = 2    /* Eq. 23 by quadrature (NEXT-2, the paper's slow integral
+                                      form; reading C12: composite 12-node Gauss-Legendre on
+                                      max(64, 4|chi|L/2pi) equal panels rounded up to 2^k)       */ };
 
 enum { ISRS_EGN_FLAG_UNIT_LINK = 1u, /* test hook: Y := 1 (oracle pin P6)                    */
        ISRS_EGN_FLAG_NO_CHAIN = 2u,  /* evaluate every span's segment sum (Eq. 8) on its own

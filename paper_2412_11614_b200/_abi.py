@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("ISRS_EGN_LIB") or os.path.join(_HERE, "libisrs_egn.so")
 
 OK, EINVAL, EOVERLAP, ERANGE, ENOMEM, ECUDA, EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
-MU_SEGMENT, MU_MACLAURIN = 0, 1
+MU_SEGMENT, MU_MACLAURIN, MU_INTEGRAL = 0, 1, 2
 FLAG_UNIT_LINK = 1
 FLAG_NO_CHAIN = 2
 FLAG_DEDUP = 4

@@ -83,6 +83,8 @@ struct isrs_egn {
   DevBuf<double> d_A2, d_A3, d_Eh, d_ah, d_gh, d_macc, d_aL;
   DevBuf<int> d_K, d_cls, d_Kc, d_chain_s0, d_chain_g;
   DevBuf<double> d_lnc_L, d_zeta_L, d_lgA, d_lgB, d_lgC, d_lgD;
+  DevBuf<double> d_Ls, d_alpha, d_gamma, d_pcr;
+  double gl_x[12], gl_w[12];
   int n_chain = 0;
   std::vector<int> chain_g, k_s;
   DevBuf<double> d_lnA, d_zeta;
@@ -133,7 +135,8 @@ static int validate(const isrs_egn_problem* p, const isrs_egn_numerics* n) {
       (n->mu_mode != ISRS_EGN_MU_SEGMENT || n->precision == 32 || (n->flags & ISRS_EGN_FLAG_DEDUP)))
     return fail(ISRS_EGN_EUNSUPPORTED, "LITERAL_GAIN is an fp64 segment-mode variant (no DEDUP)");
   if (n->f_samples < 0 || n->f_samples > 4096) return fail(ISRS_EGN_EINVAL, "f_samples must be in [0, 4096]");
-  if (n->mu_mode != ISRS_EGN_MU_SEGMENT && n->mu_mode != ISRS_EGN_MU_MACLAURIN)
+  if (n->mu_mode != ISRS_EGN_MU_SEGMENT && n->mu_mode != ISRS_EGN_MU_MACLAURIN &&
+      n->mu_mode != ISRS_EGN_MU_INTEGRAL)
     return fail(ISRS_EGN_EUNSUPPORTED, "unknown mu_mode");
   const double lim = 4.0e15;  // |values| < 2^52: integer-Hz arithmetic exact
   for (int i = 0; i < p->n_ch; ++i) {
@@ -177,6 +180,29 @@ static int validate(const isrs_egn_problem* p, const isrs_egn_numerics* n) {
 
 static int cuda_fail(cudaError_t e, const char* what) {
   return fail(ISRS_EGN_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// 12-point Gauss-Legendre rule on [-1, 1] (integral form, reading C12): roots of P_12 by Newton
+// iteration from the Chebyshev-like guesses cos(pi (i + 3/4) / (n + 1/2)); w = 2 / ((1 - x^2) P'_12^2).
+static void gauss_legendre12(double* x, double* w) {
+  const int n = 12;
+  for (int i = 0; i < n; ++i) {
+    double t = std::cos(M_PI * (i + 0.75) / (n + 0.5)), dp = 0.0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = t;                    // Bonnet recurrence
+      for (int k = 2; k <= n; ++k) {
+        const double p2 = ((2.0 * k - 1.0) * t * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = n * (t * p1 - p0) / (t * t - 1.0);
+      const double dt = p1 / dp;
+      t -= dt;
+      if (std::fabs(dt) < 1e-17) break;
+    }
+    x[n - 1 - i] = t;                              // ascending order
+    w[n - 1 - i] = 2.0 / ((1.0 - t * t) * dp * dp);
+  }
 }
 
 // Host-side canonicalisation of the channel plan (reading C5): offsets from the occupied-band
@@ -302,6 +328,14 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
     const double x = h->b_tot * zL[s];
     lncL[s] = (x == 0.0) ? 0.0 : std::log(x / (2.0 * std::sinh(0.5 * x)));   // Eq. 14
   }
+  std::vector<double> vL(ns), vA(ns), vG(ns), vP(ns);
+  for (int s = 0; s < ns; ++s) {
+    vL[s] = p->length_m[s];
+    vA[s] = p->alpha_per_m[s];
+    vG[s] = p->gamma_per_w_m[s];
+    vP[s] = h->p_tot * p->cr_per_w_m_hz[s];
+  }
+  gauss_legendre12(h->gl_x, h->gl_w);
   for (int s = 1; s < ns; ++s) {
     lgA[s] = lgA[s - 1] + 3.0 * lncL[s - 1];
     lgB[s] = lgB[s - 1] + zL[s - 1];
@@ -335,7 +369,8 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
             h->d_macc.upload(macc) && h->d_aL.upload(aL) && h->d_K.upload(K) && h->d_cls.upload(cls) &&
             h->d_Kc.upload(cK) && h->d_chain_s0.upload(ch_s0) && h->d_chain_g.upload(ch_g) &&
             h->d_lnc_L.upload(lncL) && h->d_zeta_L.upload(zL) && h->d_lgA.upload(lgA) &&
-            h->d_lgB.upload(lgB) && h->d_lgC.upload(lgC) && h->d_lgD.upload(lgD);
+            h->d_lgB.upload(lgB) && h->d_lgC.upload(lgC) && h->d_lgD.upload(lgD) &&
+            h->d_Ls.upload(vL) && h->d_alpha.upload(vA) && h->d_gamma.upload(vG) && h->d_pcr.upload(vP);
   DevBuf<double> dL, dA, dC;
   ok = ok && dL.upload(cL) && dA.upload(cA) && dC.upload(cC) &&
        h->d_lnA.alloc((size_t)h->n_cls * h->kstride) && h->d_zeta.alloc((size_t)h->n_cls * h->kstride);
@@ -544,14 +579,18 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
   kp.chain_s0 = h->d_chain_s0.p; kp.chain_g = h->d_chain_g.p; kp.n_chain = h->n_chain;
   kp.lnc_L = h->d_lnc_L.p; kp.zeta_L = h->d_zeta_L.p; kp.lgA = h->d_lgA.p; kp.lgB = h->d_lgB.p;
   kp.lgC = h->d_lgC.p; kp.lgD = h->d_lgD.p;
+  kp.Ls = h->d_Ls.p; kp.alpha = h->d_alpha.p; kp.gamma = h->d_gamma.p; kp.pcr = h->d_pcr.p;
+  kp.b_tot = h->b_tot;
+  for (int i = 0; i < 12; ++i) { kp.gl_x[i] = h->gl_x[i]; kp.gl_w[i] = h->gl_w[i]; }
   kp.lnA = h->d_lnA.p; kp.zeta = h->d_zeta.p; kp.Kc = h->d_Kc.p; kp.n_cls = h->n_cls;
   kp.kstride = h->kstride; kp.tstride = h->tstride; kp.tw = h->tw; kp.N = h->N;
   kp.fv = h->d_fv.p; kp.desc = h->d_desc.p; kp.partials = h->d_partials.p;
   kp.mode = (h->num.flags & ISRS_EGN_FLAG_UNIT_LINK) ? MODE_UNIT
+            : (h->num.mu_mode == ISRS_EGN_MU_INTEGRAL ? MODE_QUAD
             : (h->num.mu_mode == ISRS_EGN_MU_MACLAURIN ? MODE_MACLAURIN
                : (h->num.precision == 32 ? MODE_SEG32
                   : ((h->num.flags & ISRS_EGN_FLAG_DEDUP) ? MODE_SEGDD
-                     : ((h->num.flags & ISRS_EGN_FLAG_LITERAL_GAIN) ? MODE_SEGLG : MODE_SEGMENT))));
+                     : ((h->num.flags & ISRS_EGN_FLAG_LITERAL_GAIN) ? MODE_SEGLG : MODE_SEGMENT)))));
   if (!h->ev[0]) {
     for (auto& e : h->ev)
       if (cudaEventCreate(&e) != cudaSuccess) return cuda_fail(cudaGetLastError(), "cudaEventCreate");

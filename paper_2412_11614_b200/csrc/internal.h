@@ -46,7 +46,7 @@ enum : int { NEED_E = 1, NEED_F = 2, NEED_G = 4, NEED_H = 8, FV_SHIFT = 8 };
 // MODE_SEGDD: the segment form with span-class dedup (NEXT-4a, ISRS_EGN_FLAG_DEDUP)
 // MODE_SEGLG: the segment form with the literal gain products of Eq. 22 (NEXT-4b)
 enum : int { MODE_SEGMENT = 0, MODE_MACLAURIN = 1, MODE_UNIT = 2, MODE_SEG32 = 3, MODE_SEGDD = 4,
-             MODE_SEGLG = 5 };
+             MODE_SEGLG = 5, MODE_QUAD = 6 };
 
 struct RegionDesc {
   int kappa, k1, k2, flags;
@@ -90,6 +90,14 @@ struct KParams {
   const double* lgB;
   const double* lgC;
   const double* lgD;
+  // integral form (NEXT-2): per span L, alpha, gamma, P_tot C_r; B_tot; Gauss-Legendre rule
+  const double* Ls;
+  const double* alpha;
+  const double* gamma;
+  const double* pcr;
+  double b_tot;
+  double gl_x[12];
+  double gl_w[12];
   // span classes: envelope a'_k(f3) = exp(lnA[c][k] - zeta[c][k] f3)
   const double* lnA;    // [n_cls][kstride]  ln(c_k) - alpha h k
   const double* zeta;   // [n_cls][kstride]

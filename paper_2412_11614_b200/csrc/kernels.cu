@@ -480,6 +480,52 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
           const double A2 = __ldg(p.A2 + s), A3 = __ldg(p.A3 + s);
           const double Eh = __ldg(p.Eh + s), ah = __ldg(p.ah + s), gh = __ldg(p.gh + s);
           const int Ks = __ldg(p.K + s);
+          if (MODE == MODE_QUAD) {
+            // ---- NEXT-2: Eq. 23 mu_s = int_0^L rho_s(z, f3) e^{i chi z} dz by the oracle's rule
+            // (reading C12): n = max(64, 4|chi|L/2pi) equal panels rounded up to 2^k, 12-node
+            // Gauss-Legendre each; rho_s from Eq. 25 evaluated at every node (the paper's slow
+            // baseline: cost grows with the oscillation |chi| L).  Points run one at a time.
+            const double Lsp = __ldg(p.Ls + s), al = __ldg(p.alpha + s), gam = __ldg(p.gamma + s);
+            const double pcr = __ldg(p.pcr + s);
+            for (int q = 0; q < PPT; ++q) {
+              const double xq = uv[q] * fma(A3, Ssum[q], A2);       // chi h / pi
+              const double xk = xq * Ks;                            // chi L / pi
+              double mr = 0.0, mi = 0.0;
+              if (valid[q]) {
+                const double want = fmax(64.0, ceil(2.0 * fabs(xk)));   // 4 |chi| L / (2 pi)
+                long long npan = 64;
+                while ((double)npan < want) npan <<= 1;
+                const double hp = Lsp / (double)npan, hh = 0.5 * hp;
+                const double xz = xk / Lsp;                         // chi / pi per metre
+                for (long long j = 0; j < npan; ++j) {
+                  const double z0 = (double)j * hp;
+#pragma unroll
+                  for (int gq = 0; gq < 12; ++gq) {
+                    const double z = fma(p.gl_x[gq] + 1.0, hh, z0);
+                    const double ze = pcr * (-expm1(-al * z)) / al;          // Eq. 2: zeta(z)
+                    const double xx = p.b_tot * ze;
+                    // Eq. 25: B P C L_eff e^{-alpha z - zeta f3} / (2 sinh(x/2)), x = B zeta
+                    const double c = (xx == 0.0) ? 1.0 : xx / (-expm1(-xx));
+                    const double rho = c * exp(-0.5 * xx - ze * f3l - al * z);
+                    double sz, cz;
+                    sincospi_d(xz * z, &sz, &cz);                  // e^{i chi z} (Eq. 24)
+                    const double wr = p.gl_w[gq] * rho;
+                    mr = fma(wr, cz, mr);
+                    mi = fma(wr, sz, mi);
+                  }
+                }
+                mr *= hh * gam;
+                mi *= hh * gam;
+              }
+              double ps = 0.0, pc = 1.0;
+              if (ch > 0) sincospi_d(th[q], &ps, &pc);
+              yr[q] = fma(mr, pc, fma(-mi, ps, yr[q]));
+              yi[q] = fma(mr, ps, fma(mi, pc, yi[q]));
+              const double t2 = fma(xq, (double)Ks, th[q]);
+              th[q] = t2 - 2.0 * rint(0.5 * t2);
+            }
+            continue;
+          }
           if (MODE == MODE_SEG32) {
             // ---- row a8: mixed fp32 variant (no span chains).  chi h / pi and its reduction
             // mod 2 stay fp64 (exact); z = cis(pi r) by sincospif; the recurrence runs on pairs
@@ -818,6 +864,7 @@ int launch_integrand(const KParams& p, const int* list, long long n_list, bool c
     if (p.mode == MODE_SEG32) return launch_one<true, MODE_SEG32>(p, list, n_list, st);
     if (p.mode == MODE_SEGDD) return launch_one<true, MODE_SEGDD>(p, list, n_list, st);
     if (p.mode == MODE_SEGLG) return launch_one<true, MODE_SEGLG>(p, list, n_list, st);
+    if (p.mode == MODE_QUAD) return launch_one<true, MODE_QUAD>(p, list, n_list, st);
     if (p.mode == MODE_MACLAURIN) return launch_one<true, MODE_MACLAURIN>(p, list, n_list, st);
     return launch_one<true, MODE_UNIT>(p, list, n_list, st);
   }
@@ -825,6 +872,7 @@ int launch_integrand(const KParams& p, const int* list, long long n_list, bool c
   if (p.mode == MODE_SEG32) return launch_one<false, MODE_SEG32>(p, list, n_list, st);
   if (p.mode == MODE_SEGDD) return launch_one<false, MODE_SEGDD>(p, list, n_list, st);
   if (p.mode == MODE_SEGLG) return launch_one<false, MODE_SEGLG>(p, list, n_list, st);
+  if (p.mode == MODE_QUAD) return launch_one<false, MODE_QUAD>(p, list, n_list, st);
   if (p.mode == MODE_MACLAURIN) return launch_one<false, MODE_MACLAURIN>(p, list, n_list, st);
   return launch_one<false, MODE_UNIT>(p, list, n_list, st);
 }

@@ -16,7 +16,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 from oracle import egn, fwm  # noqa: E402
-from workloads import bj_config, tiny_link  # noqa: E402
+from workloads import bj_config, paper_analog, tiny_link  # noqa: E402
 
 EPS = np.finfo(np.float64).eps
 TOL_ETA = 1e-10
@@ -271,6 +271,29 @@ def test_literal_gain_chained_matches_unchained_c2(isrs):
     a, _ = gpu_eta(isrs, link, coi=[0, 19, 39], flags=isrs.FLAG_LITERAL_GAIN)
     b, _ = gpu_eta(isrs, link, coi=[0, 19, 39], flags=isrs.FLAG_LITERAL_GAIN | isrs.FLAG_NO_CHAIN)
     assert np.all(np.abs(a - b) / b <= TOL_ETA), np.abs(a - b) / b
+
+
+@pytest.mark.parametrize("name", ["uniform_64gbd_2span", "strong_isrs", "mixed_rates_guard"])
+def test_integral_form_parity_tiny(isrs, name):
+    """NEXT-2: GPU Eq. 23 by the oracle's quadrature rule (C12) against oracle quad mode."""
+    link = tiny_link(**TINY[name])
+    e_o, _ = egn.eta(link, mu_mode="quad")
+    e_g, _ = gpu_eta(isrs, link, mu_mode=isrs.MU_INTEGRAL)
+    assert np.all(np.abs(e_g - e_o) / e_o <= TOL_ETA), (name, np.abs(e_g - e_o) / e_o)
+
+
+def test_integral_form_vs_segment_pa_ir(isrs):
+    """P4 on the GPU at the paper's reduced Table-I analog (Delta-rho ~ 8.2 dB): the segment closed
+    form (dz = 1 km) stays within the paper's MAE < 0.001 dB of the integral form, and the
+    GPU integral form matches the oracle's quad mode on the sampled COIs."""
+    link = paper_analog("Ir", fmt="qpsk")
+    coi = [0, 7, 14]
+    quad, _ = gpu_eta(isrs, link, coi=coi, mu_mode=isrs.MU_INTEGRAL)
+    seg, _ = gpu_eta(isrs, link, coi=coi)
+    err = np.abs(10 * np.log10(seg) - 10 * np.log10(quad))
+    assert err.mean() < 1e-3 and err.max() < 2.7e-3, err
+    e_o, _ = egn.eta(link, coi=[7], mu_mode="quad")
+    assert abs(quad[1] - e_o[0]) / e_o[0] <= TOL_ETA
 
 
 DB_TOL_FP32 = 1e-3     # north star: optional fp32 path within 0.001 dB
