@@ -57,6 +57,25 @@ def algorithmic_work_per_point(chain_g, k_s):
     return flops, slots
 
 
+def ncu_traffic():
+    """DRAM bytes (read + write) per launch of the D-only integrand kernel from the newest committed
+    `ncu --set full` summary under profiles/ (tools/ncu_summary.py), or (None, None)."""
+    import glob
+    best = None
+    for fn in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_integrand*.json"))):
+        if "fp32" in fn:
+            continue
+        try:
+            with open(fn) as fh:
+                d = json.load(fh)
+            for k in (d.get("kernels", []) if isinstance(d, dict) else []):
+                if "integrand_kernel<0, 0>" in (k.get("kernel") or "") and "dram_traffic_bytes" in k:
+                    best = (float(k["dram_traffic_bytes"]), os.path.relpath(fn, ROOT))
+        except (OSError, ValueError):
+            continue
+    return best if best else (None, None)
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -118,8 +137,15 @@ def dist_setup(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch.distributed as dist
-        backend = "nccl" if args.impl == "ours" else "gloo"
+        backend = args.backend or ("nccl" if args.impl == "ours" else "gloo")
         dist.init_process_group(backend)
+    if args.impl == "ours":
+        import torch
+        ndev = torch.cuda.device_count()
+        if ndev and local >= ndev:
+            # more ranks than GPUs (functional test of the multi-rank path only; the driver runs
+            # one rank per GPU): ranks share devices round-robin
+            local = local % ndev
     return ws, rank, local
 
 
@@ -214,8 +240,8 @@ def run_ours(args, link, ws, rank, local):
         # per-COI sums [n, 6] are all-gathered over NCCL (NVLink/NVSwitch) and every rank combines
         # them in fixed rank order -> the same eta on every rank (strong scaling of one link).
         import torch.distributed as dist
-        sums = torch.empty((n, 6), dtype=torch.float64, device=dev)
-        gathered = torch.empty((ws, n, 6), dtype=torch.float64, device=dev)
+        sums = torch.empty(n * 6, dtype=torch.float64, device=dev)          # flat: any backend
+        gathered = torch.empty(ws * n * 6, dtype=torch.float64, device=dev)
 
         def step():
             eng.nli_shard_into(rank, ws, sums.data_ptr(), None, stream.cuda_stream)
@@ -266,6 +292,12 @@ def run_ours(args, link, ws, rank, local):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms_max = float(t.item())
     eta_host = eta.cpu().numpy()
+    same_eta = None
+    if ws > 1:       # every rank combined the same gathered sums in the same order: bitwise equal
+        ge = torch.empty(ws * n, dtype=torch.float64, device=dev)
+        torch.distributed.all_gather_into_tensor(ge, eta)
+        ge = ge.cpu().numpy().reshape(ws, n)
+        same_eta = bool(all(np.array_equal(ge[0], ge[r]) for r in range(ws)))
 
     # roofline of the dominant kernel (integrand over D-only regions)
     kd_ms = float(np.mean([k[0][0] for k in kern_ms]))
@@ -277,6 +309,7 @@ def run_ours(args, link, ws, rank, local):
     ach = ps_d * fpp / (kd_ms * 1e-3) / 1e12
     peak = fp64_peak_tflops()
     slots_ach = ps_d * spp / (kd_ms * 1e-3) / 1e12
+    traffic, traffic_src = ncu_traffic()
     slots_peak = SMS * FP64_LANES * SM_MAX_MHZ * 1e6 / 1e12
 
     # end to end through the public API with host buffers: create + nli + D2H + destroy
@@ -291,10 +324,10 @@ def run_ours(args, link, ws, rank, local):
             t0 = time.perf_counter()
             if ws > 1:
                 with isrs.Engine(link, device=local, precision=args.precision) as e2:
-                    s2 = e2.nli_shard(rank, ws)
-                    g2 = torch.empty((ws, n, 6), dtype=torch.float64, device=dev)
+                    s2 = e2.nli_shard(rank, ws).reshape(-1)
+                    g2 = torch.empty(ws * n * 6, dtype=torch.float64, device=dev)
                     torch.distributed.all_gather_into_tensor(g2, s2)
-                    e2.combine(g2).cpu()
+                    e2.combine(g2.reshape(ws, n, 6)).cpu()
             else:
                 isrs.eta_host(link, device=local, precision=args.precision)
             dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
@@ -340,7 +373,7 @@ def run_ours(args, link, ws, rank, local):
                 "point_spans_per_step": pspans, "points_per_step": pts, "regions_per_step": nreg,
                 "kernel_ms": {"integrand_D": kd_ms, "integrand_coherent": kc_ms, "reduce": kr_ms},
                 "roofline": {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                             "frac": ach / peak, "traffic": None,
+                             "frac": ach / peak, "traffic": traffic, "traffic_source": traffic_src,
                              "kernel": "isrs::integrand_kernel<false,0> (D-only regions)",
                              "flops_per_point_span": fpp,
                              "span_chains": [int(g) for g in chain_g],
@@ -354,6 +387,8 @@ def run_ours(args, link, ws, rank, local):
                 "gpu_launches": launches_per_step * args.steps,
                 "clocks": clk, "e2e": e2e,
                 "eta_db_first_mid_last": [float(10 * np.log10(eta_host[i])) for i in (0, n // 2, n - 1)]}
+        if same_eta is not None:
+            line["eta_bitwise_equal_across_ranks"] = same_eta
         if dedup is not None:
             line["dedup_effective"] = dedup
         if not args.no_cpu and ws == 1:
@@ -373,6 +408,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32],
                     help="64: the fp64 hot path (default); 32: the mixed fp32 variant (row a8)")
+    ap.add_argument("--backend", default=None, help="torch.distributed backend (default nccl)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dedup", action="store_true", help="skip the separate NEXT-4a dedup timing")

@@ -181,6 +181,25 @@ __global__ void __launch_bounds__(128, 4) kern(double* out, long long* cyc, int 
           b2[p4 + 2] = b1[p4 + 2]; b1[p4 + 2] = n2;
           b2[p4 + 3] = b1[p4 + 3]; b1[p4 + 3] = n3;
         }
+      } else if (V == 32) {  // block split: one point, 4 chains sharing c2[0]; coefficient
+        // streams at two offsets (chains 0,2 / 1,3), two 16-byte loads per pair of steps
+        const double2 ta = rowp[i2 & 31], tb = rowp[(i2 + 20) & 31];
+#pragma unroll
+        for (int p4 = 0; p4 < PPT; p4 += 4) {
+          const double c = c2[p4];
+          const double n0 = fma(c, b1[p4 + 0], ta.x - b2[p4 + 0]);
+          const double n1 = fma(c, b1[p4 + 1], tb.x - b2[p4 + 1]);
+          const double n2 = fma(c, b1[p4 + 2], ta.x - b2[p4 + 2]);
+          const double n3 = fma(c, b1[p4 + 3], tb.x - b2[p4 + 3]);
+          const double m0 = fma(c, n0, ta.y - b1[p4 + 0]);
+          const double m1_ = fma(c, n1, tb.y - b1[p4 + 1]);
+          const double m2 = fma(c, n2, ta.y - b1[p4 + 2]);
+          const double m3 = fma(c, n3, tb.y - b1[p4 + 3]);
+          b2[p4 + 0] = n0; b1[p4 + 0] = m0;
+          b2[p4 + 1] = n1; b1[p4 + 1] = m1_;
+          b2[p4 + 2] = n2; b1[p4 + 2] = m2;
+          b2[p4 + 3] = n3; b1[p4 + 3] = m3;
+        }
       } else if (V == 8) {   // independent 1 DADD : 3 DFMA
 #pragma unroll
         for (int q = 0; q < PPT; ++q) { b1[q] = b1[q] - tc.x; b2[q] = fma(b2[q], cs, tc.y); c2[q] = fma(c2[q], cs, tc.x); tc.y = fma(tc.y, cs, tc.x); }
@@ -237,6 +256,8 @@ int main() {
   cudaMalloc(&d, 8);
   cudaMalloc(&dc, 3 * 8 * 8192);
   const int n = p.multiProcessorCount;
+  run<32, 4>("Q block split, 1 point", n, d, dc);
+  run<32, 8>("Q block split, 2 points", n, d, dc);
   run<31, 4>("R4 residue split, 1 point", n, d, dc);
   run<31, 8>("R4 residue split, 2 points", n, d, dc);
   run<30, 4>("S even/odd shared c2w", n, d, dc);
