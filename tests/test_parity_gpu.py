@@ -69,6 +69,34 @@ def test_eta_parity_tiny(isrs, name):
     assert np.all(np.abs(t_g - t_o) <= TOL_ETA * scale), (name, t_g, t_o)
 
 
+EDGE = {
+    # N = 2 (the smallest even grid), one channel
+    "min_grid_N2": (dict(n_ch=1, rates_gbd=(64,), n_span=2, grid_n=2, fmts=("qpsk",)), {}),
+    # N = 1024 single channel: the largest grid the oracle finishes in seconds (1 M points)
+    "big_grid_N1024": (dict(n_ch=1, rates_gbd=(64,), n_span=1, grid_n=1024, fmts=("16qam",)), {}),
+    # J = 2N - 1 = 519 lattice lines > LINE_CAP = 512: two line segments per region
+    "two_line_segments_N260": (dict(n_ch=2, rates_gbd=(65,), spacing_ghz=100.0, n_span=1, grid_n=260,
+                                    fmts=("qpsk",)), {}),
+    # odd K (dz = 1100 m -> K = 73): no chains, odd-length recurrence
+    "odd_K73": (dict(n_ch=3, rates_gbd=(64,), n_span=3, grid_n=8, fmts=("16qam",)), {"delta_z_m": 1100.0}),
+    # K = 800 (dz = 100 m): only 3 table rows fit the envelope table, frequent rebuilds
+    "large_K800": (dict(n_ch=2, rates_gbd=(64,), n_span=2, grid_n=8, fmts=("64qam",)), {"delta_z_m": 100.0}),
+}
+
+
+@pytest.mark.parametrize("name", sorted(EDGE))
+def test_eta_parity_edge_cases(isrs, name):
+    kw, num = EDGE[name]
+    link = tiny_link(**kw)
+    if "delta_z_m" in num:
+        link = link.with_(delta_z_m=num["delta_z_m"])
+    e_o, t_o = egn.eta(link)
+    e_g, t_g = gpu_eta(isrs, link)
+    assert np.all(np.abs(e_g - e_o) / e_o <= TOL_ETA), (name, np.abs(e_g - e_o) / e_o)
+    scale = np.abs(t_o).sum(axis=1, keepdims=True)
+    assert np.all(np.abs(t_g - t_o) <= TOL_ETA * scale), name
+
+
 def test_eta_parity_c1_full(isrs):
     link = bj_config("c1")
     e_o, t_o = egn.eta(link)
