@@ -596,6 +596,12 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
       if (cudaEventCreate(&e) != cudaSuccess) return cuda_fail(cudaGetLastError(), "cudaEventCreate");
   }
   int launches = 0;
+#ifdef ISRS_PROF
+  static unsigned long long* d_prof = nullptr;
+  if (!d_prof) cudaMalloc(&d_prof, 8 * sizeof(unsigned long long));
+  cudaMemsetAsync(d_prof, 0, 8 * sizeof(unsigned long long), st);
+  kp.prof = d_prof;
+#endif
   cudaEventRecord(h->ev[0], st);
   if (launch_integrand(kp, dl_d, (long long)h->act_d.size(), false, st, &launches) != 0)
     return cuda_fail(cudaGetLastError(), "integrand launch (D-only regions)");
@@ -611,6 +617,20 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
              part_out};
   if (launch_reduce(rp, st) != 0) return cuda_fail(cudaGetLastError(), "reduce launch");
   cudaEventRecord(h->ev[3], st);
+#ifdef ISRS_PROF
+  {
+    unsigned long long hp[8];
+    cudaMemcpyAsync(hp, d_prof, sizeof(hp), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    double tot = 0;
+    for (int i = 0; i < 7; ++i) tot += (double)hp[i];
+    const char* nm[7] = {"prologue", "line scan", "chunk setup", "table build", "span math",
+                         "accumulate", "epilogue"};
+    fprintf(stderr, "ISRS_PROF warp-cycles:");
+    for (int i = 0; i < 7; ++i) fprintf(stderr, " %s %.2f%%", nm[i], 100.0 * hp[i] / tot);
+    fprintf(stderr, " (total %.3e)\n", tot);
+  }
+#endif
   launches += 1;
   h->last_launches = launches;
   h->last_stream = st;

@@ -112,6 +112,7 @@ struct KParams {
   const RegionDesc* desc;
   double* partials;     // [n_regions][6]: D_w, E_w, F_w, G_w, H_w, n_points
   int mode;
+  unsigned long long* prof;   // ISRS_PROF builds only: per-phase warp-cycle counters [8]
 };
 
 struct RParams {

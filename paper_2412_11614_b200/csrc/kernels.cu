@@ -32,6 +32,16 @@
 #ifndef ISRS_UNROLL
 #define ISRS_UNROLL 4
 #endif
+#ifdef ISRS_PROF
+// phase timers (debug builds only, -DISRS_PROF): per-warp clock64 deltas summed into p.prof
+#define PROF_DECL unsigned long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long prof_t = clock64();
+#define PROF_MARK(i) { const long long t_ = clock64(); prof_acc[i] += (unsigned long long)(t_ - prof_t); prof_t = t_; }
+#define PROF_FLUSH if ((threadIdx.x & 31) == 0 && p.prof) { for (int i_ = 0; i_ < 8; ++i_) atomicAdd(p.prof + i_, prof_acc[i_]); }
+#else
+#define PROF_DECL
+#define PROF_MARK(i)
+#define PROF_FLUSH
+#endif
 #define ISRS_STR(x) #x
 #define ISRS_UNROLL_PRAGMA(n) _Pragma(ISRS_STR(unroll n))
 
@@ -289,6 +299,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
   Smem sm;
   smem_layout(p.tstride, p.tw, p.N, COH, smem_raw, &sm);
   const int tid = threadIdx.x;
+  PROF_DECL
   const int rid = list[blockIdx.x];
   const RegionDesc rd = p.desc[rid];
   const int k1 = rd.k1, k2 = rd.k2, flags = rd.flags;
@@ -321,6 +332,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
     }
   }
 
+  PROF_MARK(0)   // prologue
   for (int seg0 = 0; seg0 < J; seg0 += LINE_CAP) {
     const int nl = min(LINE_CAP, J - seg0);
     // ---- line scan: each thread owns LPT consecutive lines (order-preserving compaction)
@@ -384,6 +396,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
     if (NP == 0) continue;
 
     int tb = 0, tn = 0, tcls = -1;  // resident table: compacted lines [tb, tb + tn), class tcls
+    PROF_MARK(1)   // line scan + compaction
     for (int p0 = 0; p0 < NP;) {
       // ---- chunk boundaries (block-uniform)
       const int i_first = line_of(sm.sl_start, S, p0);
@@ -433,8 +446,10 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
         th[q] = 0.0;
       }
 
+      PROF_MARK(2)   // chunk setup (line lookup, geometry)
       if (MODE != MODE_UNIT) {
         for (int ch = 0; ch < p.n_chain; ++ch) {
+          if (ch > 0) { PROF_MARK(4) }   // previous chain's span math
           // chain of G identical consecutive spans starting at s (G = 1 unless chained, R9)
           const int s = __ldg(p.chain_s0 + ch), G = __ldg(p.chain_g + ch);
           const int cls = __ldg(p.cls + s);
@@ -476,6 +491,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
             }
             __syncthreads();
           }
+          PROF_MARK(3)   // table (re)build incl. barriers
           if (!wact) continue;   // warp-uniform: idle warps of a ragged last chunk skip the math
           const double A2 = __ldg(p.A2 + s), A3 = __ldg(p.A3 + s);
           const double Eh = __ldg(p.Eh + s), ah = __ldg(p.ah + s), gh = __ldg(p.gh + s);
@@ -742,6 +758,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
         }
       }
 
+      PROF_MARK(4)   // span math (z, recurrence, mu, Y)
       // ---- D accumulation
 #pragma unroll
       for (int q = 0; q < PPT; ++q) {
@@ -821,6 +838,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
     __syncthreads();
   }
 
+  PROF_MARK(5)   // D / coherent accumulation, chunk tails
   const double Dsum = block_sum(Dacc, sm.red);
   if (tid == 0) {
     double* out = p.partials + (size_t)rid * 6;
@@ -838,6 +856,8 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
     out[4] = (COH && (flags & NEED_H)) ? (hsum.x * hsum.x + hsum.y * hsum.y) * (d1 * d2) * (d1 * d2) : 0.0;
     out[5] = (double)npts_total;
   }
+  PROF_MARK(6)   // epilogue (block sum, partials)
+  PROF_FLUSH
 }
 
 template <bool COH, int MODE>

@@ -1,3 +1,4 @@
-mkdir -p gpurun_out/r01r
-python -m pytest tests -m gpu -x -q > gpurun_out/r01r/pytest.log 2>&1; tail -2 gpurun_out/r01r/pytest.log
-python tools/run_configs.py --configs c2,c4 > gpurun_out/r01r/configs.jsonl 2>&1; cut -c1-300 gpurun_out/r01r/configs.jsonl
+mkdir -p gpurun_out/r01t
+python tools/perf_variants.py build_variants/lib_*.so --config=c4 --coi=0,40,79 --reps=2 > gpurun_out/r01t/variants_c4.txt 2>&1
+python tools/perf_variants.py build_variants/lib_*.so --config=c2 --reps=2 > gpurun_out/r01t/variants_c2.txt 2>&1
+cat gpurun_out/r01t/variants_c4.txt gpurun_out/r01t/variants_c2.txt
