@@ -193,9 +193,8 @@ __device__ inline double block_sum(double v, double* red) {
   return r;
 }
 
-// index i with sl_start[i] <= p < sl_start[i+1], searched in [lo, S-1]
-__device__ inline int line_of(const int* sl_start, int S, int p, int lo = 0) {
-  int hi = S - 1;
+// index i with sl_start[i] <= p < sl_start[i+1], searched in [lo, hi]
+__device__ inline int line_of(const int* sl_start, int hi, int p, int lo = 0) {
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
     if (sl_start[mid] <= p) lo = mid; else hi = mid - 1;
@@ -397,12 +396,12 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
 
     int tb = 0, tn = 0, tcls = -1;  // resident table: compacted lines [tb, tb + tn), class tcls
     PROF_MARK(1)   // line scan + compaction
+    int i_first = 0;                // line of slot p0 (carried across chunks: no search)
     for (int p0 = 0; p0 < NP;) {
       // ---- chunk boundaries (block-uniform)
-      const int i_first = line_of(sm.sl_start, S, p0);
       const int lim = min(i_first + p.tw, S);
       const int p_end = min(p0 + CP, sm.sl_start[lim]);
-      const int i_last = line_of(sm.sl_start, S, p_end - 1);
+      const int i_last = line_of(sm.sl_start, lim - 1, p_end - 1, i_first);
 
       // ---- per-thread points: PPT consecutive slots of one line (lines are padded to whole
       // groups), so one envelope-table row serves all PPT recurrences of the thread
@@ -415,7 +414,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
       const int lane = tid & 31;
       const int wslot0 = p0 + PPT * (tid & ~31);
       const bool wact = wslot0 < p_end;                    // warp has at least one valid group
-      const int i0 = wact ? line_of(sm.sl_start, S, wslot0, i_first) : i_first;
+      const int i0 = wact ? line_of(sm.sl_start, i_last, wslot0, i_first) : i_first;
       int pos = 32;
       if (lane < 31 && i0 + 1 + lane < S) pos = (sm.sl_start[i0 + 1 + lane] - wslot0) / PPT;
       const unsigned starts = __reduce_or_sync(0xffffffffu, (pos < 32) ? (1u << pos) : 0u);
@@ -826,6 +825,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
         __syncthreads();
       }
       p0 = p_end;
+      i_first = (sm.sl_start[i_last + 1] <= p_end) ? i_last + 1 : i_last;
     }
     if (COH && (flags & (NEED_G | NEED_H)) && tid == 0) {
       for (int i = 0; i < S; ++i) {

@@ -1,4 +1,6 @@
-mkdir -p gpurun_out/r01t
-python tools/perf_variants.py build_variants/lib_*.so --config=c4 --coi=0,40,79 --reps=2 > gpurun_out/r01t/variants_c4.txt 2>&1
-python tools/perf_variants.py build_variants/lib_*.so --config=c2 --reps=2 > gpurun_out/r01t/variants_c2.txt 2>&1
-cat gpurun_out/r01t/variants_c4.txt gpurun_out/r01t/variants_c2.txt
+mkdir -p gpurun_out/r01u
+python -m pytest tests -m gpu -x -q > gpurun_out/r01u/pytest.log 2>&1; tail -1 gpurun_out/r01u/pytest.log
+python tools/perf_variants.py build_variants/lib_*.so --reps=3 > gpurun_out/r01u/variants_c2.txt 2>&1
+python tools/perf_variants.py build_variants/lib_*.so --config=c4 --coi=0,40,79 --reps=2 > gpurun_out/r01u/variants_c4.txt 2>&1
+python tools/perf_variants.py build_variants/lib_*.so --config=c5 --coi=100 --reps=1 > gpurun_out/r01u/variants_c5.txt 2>&1
+cat gpurun_out/r01u/variants_*.txt
