@@ -152,11 +152,13 @@ ISRS_EGN_API int isrs_egn_work(isrs_egn_t *h, int64_t *points, int64_t *point_sp
 ISRS_EGN_API int isrs_egn_eta_host(const isrs_egn_problem *p, const isrs_egn_numerics *n, int device,
                       int32_t n_coi, const int32_t *coi, double *eta_host, double *terms_host);
 
-/* Device time of each kernel of the most recent isrs_egn_nli() (CUDA events recorded on its
- * stream around each launch; synchronises): ms_out[0] = integrand over D-only regions,
- * ms_out[1] = integrand over coherent (E/F/G/H) regions, ms_out[2] = per-COI reduction; a kernel
- * that was not launched reads 0.  point_spans_out (or NULL): the point-spans each integrand
- * launch processed ([0], [1]) and their sum ([2]). */
+/* Device time of each kernel of the most recent isrs_egn_nli() (CUDA events; synchronises).
+ * The coherent-region integrand runs on an internal side stream concurrently with the D-only one
+ * (fork/join with events around the caller's stream).  ms_out[4]: [0] = D-only integrand (on the
+ * caller's stream), [1] = coherent (E/F/G/H) integrand (side stream, overlapping [0]), [2] =
+ * per-COI reduction, [3] = the whole integrand phase (both launches, fork to join); a kernel that
+ * was not launched reads 0.  point_spans_out (or NULL): the point-spans each integrand launch
+ * processed ([0], [1]) and their sum ([2]). */
 ISRS_EGN_API int isrs_egn_last_kernel_ms(isrs_egn_t *h, double *ms_out, double *point_spans_out);
 
 /* Span chains of the handle (reading R9): *n_chain chains; chain_g (or NULL, capacity n_span)

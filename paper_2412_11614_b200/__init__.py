@@ -87,8 +87,9 @@ class Engine:
         return p.value, ps.value, r.value
 
     def last_kernel_ms(self):
-        """([ms_D_only, ms_coherent, ms_reduce], [point_spans_D_only, point_spans_coherent, total])."""
-        ms = (ctypes.c_double * 3)()
+        """([ms_D_only, ms_coherent, ms_reduce, ms_integrand_phase],
+        [point_spans_D_only, point_spans_coherent, total])."""
+        ms = (ctypes.c_double * 4)()
         ps = (ctypes.c_double * 3)()
         _abi.check(_abi.get().isrs_egn_last_kernel_ms(self._h, ms, ps))
         return list(ms), list(ps)

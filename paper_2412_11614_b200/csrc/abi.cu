@@ -106,10 +106,18 @@ struct isrs_egn {
   bool have_result = false;
   int last_launches = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // coherent-region integrand on a side stream, concurrent with the D-only launch (fills its tail)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, evc[2] = {nullptr, nullptr};
   bool launched[2] = {false, false};
   ~isrs_egn() {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    for (auto& e : evc)
+      if (e) cudaEventDestroy(e);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
   }
 };
 
@@ -602,12 +610,27 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
   cudaMemsetAsync(d_prof, 0, 8 * sizeof(unsigned long long), st);
   kp.prof = d_prof;
 #endif
+  if (!h->side) {
+    if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreate(&h->evc[0]) != cudaSuccess || cudaEventCreate(&h->evc[1]) != cudaSuccess)
+      return cuda_fail(cudaGetLastError(), "side stream / events");
+  }
+  // fork: the coherent regions run on the side stream while the D-only regions run on `st`;
+  // join before the per-COI reduce.  ev[0] -> ev[2] brackets the whole integrand phase.
   cudaEventRecord(h->ev[0], st);
+  cudaEventRecord(h->ev_fork, st);
+  cudaStreamWaitEvent(h->side, h->ev_fork, 0);
+  cudaEventRecord(h->evc[0], h->side);
+  if (launch_integrand(kp, dl_c, (long long)h->act_c.size(), true, h->side, &launches) != 0)
+    return cuda_fail(cudaGetLastError(), "integrand launch (coherent regions)");
+  cudaEventRecord(h->evc[1], h->side);
+  cudaEventRecord(h->ev_join, h->side);
   if (launch_integrand(kp, dl_d, (long long)h->act_d.size(), false, st, &launches) != 0)
     return cuda_fail(cudaGetLastError(), "integrand launch (D-only regions)");
   cudaEventRecord(h->ev[1], st);
-  if (launch_integrand(kp, dl_c, (long long)h->act_c.size(), true, st, &launches) != 0)
-    return cuda_fail(cudaGetLastError(), "integrand launch (coherent regions)");
+  cudaStreamWaitEvent(st, h->ev_join, 0);
   cudaEventRecord(h->ev[2], st);
   h->launched[0] = !h->act_d.empty();
   h->launched[1] = !h->act_c.empty();
@@ -754,11 +777,17 @@ extern "C" int isrs_egn_last_kernel_ms(isrs_egn_t* h, double* ms_out, double* po
   if (!h->have_result) return fail(ISRS_EGN_EINVAL, "no isrs_egn_nli() result yet");
   cudaError_t ce = cudaEventSynchronize(h->ev[3]);
   if (ce != cudaSuccess) return cuda_fail(ce, "event sync");
-  for (int k = 0; k < 3; ++k) {
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, h->ev[k], h->ev[k + 1]);
-    ms_out[k] = (k < 2 && !h->launched[k]) ? 0.0 : (double)ms;
-  }
+  // [0] D-only launch (start of the integrand phase -> its end on st), [1] coherent launch (side
+  // stream, concurrent), [2] the per-COI reduce; [3] = the whole integrand phase (both launches)
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]);
+  ms_out[0] = h->launched[0] ? (double)ms : 0.0;
+  cudaEventElapsedTime(&ms, h->evc[0], h->evc[1]);
+  ms_out[1] = h->launched[1] ? (double)ms : 0.0;
+  cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]);
+  ms_out[2] = (double)ms;
+  cudaEventElapsedTime(&ms, h->ev[0], h->ev[2]);
+  ms_out[3] = (double)ms;
   if (point_spans_out) {
     const size_t nr = h->wl.desc.size();
     std::vector<double> np(nr);

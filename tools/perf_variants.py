@@ -17,8 +17,9 @@ for _ in range(REPS):
     e.nli(coi=coi); torch.cuda.synchronize(); ms.append(e.last_kernel_ms())
 eta = e.nli(coi=coi).cpu().numpy()
 d = float(np.median([m[0][0] for m in ms])); c = float(np.median([m[0][1] for m in ms]))
+ph = float(np.median([m[0][3] for m in ms])) if len(ms[0][0]) > 3 else d + c
 ps = ms[-1][1]
-print(json.dumps({"D_ms": d, "coh_ms": c, "ps_D": ps[0], "ps_all": ps[2], "rate_D": ps[0] / d * 1e3,
+print(json.dumps({"phase_ms": ph, "D_ms": d, "coh_ms": c, "ps_D": ps[0], "ps_all": ps[2], "rate_D": ps[0] / d * 1e3,
                   "eta0": float(eta[0])}))
 '''
 args = [a for a in sys.argv[1:] if not a.startswith("--")]

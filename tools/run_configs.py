@@ -45,7 +45,7 @@ def main():
             chain_g, k_s = e.span_chains()
         eta = eta.cpu().numpy()
         fl, sl = algorithmic_work_per_point(chain_g, k_s)
-        ach = kps[2] * fl / link.n_span / ((kms[0] + kms[1]) * 1e-3) / 1e12
+        ach = kps[2] * fl / link.n_span / (kms[3] * 1e-3) / 1e12
         print(json.dumps({
             "config": cfg, "n_ch": link.n_ch, "n_span": link.n_span, "grid_n": link.grid_n,
             "precision": a.precision, "regions": nreg, "points": pts, "point_spans": pspans,
