@@ -34,7 +34,7 @@ fi
 if [[ $STAGES == *f* ]]; then
   CMD="python tools/ncu_target.py --config c2 --reps 2"
   timeout 300 $CMD > "$OUT/plain_full.log" 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:integrand_kernel -s 2 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:integrand_kernel -s 3 -c 1 \
       -o "$OUT/prof" $CMD > "$OUT/ncu_full.log" 2>&1
   echo "ncu_full rc=$?" >> "$OUT/status"
 fi
