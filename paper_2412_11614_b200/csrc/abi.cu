@@ -171,6 +171,24 @@ static int validate(const isrs_egn_problem* p, const isrs_egn_numerics* n) {
       return fail(ISRS_EGN_EOVERLAP, "bands of channels " + std::to_string(i - 1) + " and " +
                                          std::to_string(i) + " overlap");
   }
+  // the integrand walks the lattice lines a m1 + b m2 = j of every channel pair (a:b = R1:R2 in
+  // lowest terms, (a + b)(N - 1) + 1 lines): rate ratios must be small rationals
+  {
+    std::vector<long long> rates;
+    for (int i = 0; i < p->n_ch; ++i) rates.push_back((long long)p->symbol_rate_hz[i]);
+    std::sort(rates.begin(), rates.end());
+    rates.erase(std::unique(rates.begin(), rates.end()), rates.end());
+    for (size_t i = 0; i < rates.size(); ++i)
+      for (size_t j = i + 1; j < rates.size(); ++j) {
+        long long x = rates[i], y = rates[j];
+        while (y) { const long long t = x % y; x = y; y = t; }
+        if ((rates[i] + rates[j]) / x > RATIO_MAX)
+          return fail(ISRS_EGN_EUNSUPPORTED,
+                      "symbol rates " + std::to_string(rates[i]) + " and " + std::to_string(rates[j]) +
+                          " Hz: ratio a:b in lowest terms has a + b > " + std::to_string(RATIO_MAX) +
+                          " (lattice line scan); use rates with a small common divisor ratio");
+      }
+  }
   for (int s = 0; s < p->n_span; ++s) {
     const std::string at = "[" + std::to_string(s) + "]";
     if (!is_fin(p->length_m[s]) || p->length_m[s] <= 0) return fail(ISRS_EGN_EINVAL, "length_m" + at + " <= 0");

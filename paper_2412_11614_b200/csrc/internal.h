@@ -34,6 +34,8 @@ constexpr int LPT = LINE_CAP / BLOCK;  // lattice lines scanned per thread
 // longest chained recurrence (segments): the phase of the implicit z^n drifts by <= n^2 eps
 // (fl(2 cos(chi h)) is exact to eps), 800^2 * 1.1e-16 = 7e-11 relative per point (DESIGN R9)
 constexpr int CHAIN_MAX = ISRS_CHAIN_MAX;
+// largest a + b of a channel-pair rate ratio a:b (lowest terms) the lattice line scan accepts
+constexpr long long RATIO_MAX = 64;
 static_assert(LINE_CAP % BLOCK == 0, "LINE_CAP must be a multiple of BLOCK");
 
 // region flags (reading C8: a term whose gate or weight is zero is not evaluated); bits >= 8

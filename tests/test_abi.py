@@ -68,6 +68,9 @@ def test_validation_errors_before_any_cuda(abi):
     assert rc == abi.EINVAL and "delta_z" in msg
     rc, msg, _ = _create(abi, l, precision=16)
     assert rc == abi.EUNSUPPORTED
+    odd = l.with_(symbol_rate_hz=np.array([64e9, 64e9 + 256 * 8, 64e9]))   # ratio ~ 3.1e7 : 3.1e7+1
+    rc, msg, _ = _create(abi, odd, grid_n=8)
+    assert rc == abi.EUNSUPPORTED and "ratio" in msg
     rc, msg, _ = _create(abi, l, f_samples=-1)
     assert rc == abi.EINVAL and "f_samples" in msg
     rc, msg, _ = _create(abi, l, f_samples=3)          # 64 GBd / 6 is not an integer (R3)
