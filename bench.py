@@ -63,7 +63,7 @@ def ncu_traffic():
     import glob
     best = None
     for fn in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_integrand*.json"))):
-        if "fp32" in fn or "_c4" in fn:      # other variants / configs
+        if "fp32" in fn or "_c2" not in fn:   # the bench config's capture only
             continue
         try:
             with open(fn) as fh:

@@ -41,7 +41,7 @@ def raw(rep):
     rows = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "raw", "--csv"))))
     h, units = rows[0], dict(zip(rows[0], rows[1]))
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "usecond": 1e-3,
-             "msecond": 1.0, "second": 1e3}
+             "msecond": 1.0, "second": 1e3, "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
     out = []
     for v in rows[2:]:
         d = dict(zip(h, v))
