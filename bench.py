@@ -383,7 +383,7 @@ def run_ours(args, link, ws, rank, local):
                              "flops_per_point_span": fpp,
                              "span_chains": [int(g) for g in chain_g],
                              "peak_note": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz "
-                                          "(DFMA microbenchmark on this pool: 34.1 TFLOP/s)"},
+                                          "(tools/dmma_probe.cu: a DFMA stream reaches 128 flop/SM-cycle = this peak)"},
                 "fp64_pipe_slots": {"achieved": slots_ach, "peak": slots_peak, "unit": "T slot/s",
                                     "frac": slots_ach / slots_peak, "per_point_span": spp,
                                     "note": "same algorithmic count with DFMA and DADD one FP64 "
