@@ -92,6 +92,23 @@ def test_validation_errors_before_any_cuda(abi):
     lat = l.with_(symbol_rate_hz=np.full(3, 64e9 + 2))
     rc, msg, _ = _create(abi, lat)
     assert rc == abi.EINVAL and "2 grid_n" in msg
+    # empty inputs and non-finite values
+    empty = l.with_(f_center_hz=np.zeros(0), symbol_rate_hz=np.zeros(0), launch_power_w=np.zeros(0),
+                    phi=np.zeros(0), psi=np.zeros(0))
+    rc, msg, _ = _create(abi, empty)
+    assert rc == abi.EINVAL and "n_ch" in msg
+    nospan = l.with_(length_m=np.zeros(0), alpha_per_m=np.zeros(0), beta2_s2_per_m=np.zeros(0),
+                     beta3_s3_per_m=np.zeros(0), gamma_per_w_m=np.zeros(0), cr_per_w_m_hz=np.zeros(0))
+    rc, msg, _ = _create(abi, nospan)
+    assert rc == abi.EINVAL and "n_span" in msg
+    nan = l.with_(launch_power_w=np.array([1e-3, np.nan, 1e-3]))
+    rc, msg, _ = _create(abi, nan)
+    assert rc == abi.EINVAL and "launch_power_w[1]" in msg
+    neg_cr = l.with_(cr_per_w_m_hz=np.array([2.8e-17, -1e-18]))
+    rc, msg, _ = _create(abi, neg_cr)
+    assert rc == abi.EINVAL and "cr_per_w_m_hz[1]" in msg
+    rc, msg, _ = _create(abi, l, grid_n=8192)
+    assert rc == abi.EINVAL and "4096" in msg
 
 
 def test_destroy_null_safe(abi):

@@ -97,6 +97,17 @@ def test_eta_parity_edge_cases(isrs, name):
     assert np.all(np.abs(t_g - t_o) <= TOL_ETA * scale), name
 
 
+def test_degenerate_zero_gamma_and_empty_coi(isrs):
+    """gamma = 0 in every span: Y = 0, eta = 0 exactly; an empty COI list is rejected."""
+    link = tiny_link(n_ch=3, rates_gbd=(64,), n_span=2, grid_n=8, fmts=("16qam",))
+    link = link.with_(gamma_per_w_m=np.zeros(2))
+    e_g, t_g = gpu_eta(isrs, link)
+    assert np.all(e_g == 0.0) and np.all(t_g == 0.0)
+    with isrs.Engine(link) as e:
+        with pytest.raises(isrs.IsrsEgnError):
+            e.nli(coi=[])
+
+
 def test_eta_parity_c1_full(isrs):
     link = bj_config("c1")
     e_o, t_o = egn.eta(link)
