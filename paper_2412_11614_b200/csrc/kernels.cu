@@ -9,7 +9,15 @@
 //                                 P:119-121) for every point and span, the span phased-array sum Y
 //                                 (Eq. 22, reading C3) in registers, and the D, E, F, G, H
 //                                 region reductions (Eqs. 17-21, reading C7), fixed order.
-//   reduce_kernel      (row a7)  per COI: Eq. 15 coefficients (reading C2) and Eq. 11.
+//   reduce_kernel      (row a7)  per COI: Eq. 15 coefficients (reading C2) and Eq. 11; in
+//                                 shard mode the raw per-COI sums of one rank's regions.
+//   combine_kernel     (§8(e))   gathered shard sums added in fixed rank order, Eq. 11 scale.
+//
+// integrand_kernel<COH, MODE>: COH = the region needs the coherent E/F/G/H sums (reading C8);
+// MODE = MODE_SEGMENT (the hot path, fp64, span chains R9), MODE_SEG32 (row a8, mixed fp32),
+// MODE_SEGDD (NEXT-4a span-class dedup), MODE_SEGLG (NEXT-4b literal Eq. 22 gain products),
+// MODE_MACLAURIN (NEXT-1, Eq. 4), MODE_QUAD (NEXT-2, Eq. 23 by quadrature), MODE_UNIT (Y := 1,
+// test hook for pin P6/P14).  Optional -DISRS_PROF adds per-phase warp-cycle timers.
 //
 // FP64 CUDA-core work (no tensor cores: the path is not a dense contraction).  The segment sum
 //   mu_s = I_0 * sum_k a_k w^k,  w = e^{(i chi - alpha) h},  I_0 = (w - 1)/(i chi - alpha)
