@@ -12,9 +12,9 @@ namespace isrs {
 #define ISRS_PPT 4
 #endif
 #ifndef ISRS_MINB
-#define ISRS_MINB 4
+#define ISRS_MINB 3
 #endif
-constexpr int BLOCK = ISRS_BLOCK;   // threads per CTA (4 warps; 4 CTAs per SM)
+constexpr int BLOCK = ISRS_BLOCK;   // threads per CTA (4 warps; 3 CTAs per SM, up to 168 registers)
 constexpr int PPT = ISRS_PPT;       // grid points per thread in flight (independent Goertzel chains)
 constexpr int MIN_BLOCKS = ISRS_MINB;  // __launch_bounds__ min CTAs per SM
 constexpr int CP = BLOCK * PPT;     // points per chunk
@@ -23,7 +23,7 @@ constexpr int LINE_CAP = 512;       // f3-lines compacted per segment (2N-1 <= 5
 #define ISRS_TW 64
 #endif
 #ifndef ISRS_TBYTES
-#define ISRS_TBYTES (24 * 1024)
+#define ISRS_TBYTES (32 * 1024)
 #endif
 constexpr int TW_MAX = ISRS_TW;     // envelope-table rows (f3-lines) resident in smem
 constexpr int T_BYTES = ISRS_TBYTES;  // smem budget of the envelope table

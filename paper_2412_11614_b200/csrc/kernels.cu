@@ -594,8 +594,9 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
               auto step = [&](float a) {
 #pragma unroll
                 for (int hq = 0; hq < PPT / 2; ++hq) {
-                  const float2 t = __ffma2_rn(b2[hq], neg1, make_float2(a, a));   // a - b_{k+2}
-                  const float2 n = __ffma2_rn(c2[hq], b1[hq], t);
+                  // (2cos b_{k+1} + a) - b_{k+2}: the shared a in the addend slot (operand reuse)
+                  const float2 t = __ffma2_rn(c2[hq], b1[hq], make_float2(a, a));
+                  const float2 n = __ffma2_rn(b2[hq], neg1, t);
                   b2[hq] = b1[hq];
                   b1[hq] = n;
                 }
@@ -676,12 +677,17 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
               ISRS_UNROLL_PRAGMA(ISRS_UNROLL)
               for (int i2 = 0; i2 < nit; ++i2) {
                 const double2 tn = rowp[i2 + 1];
+                // b_k = (2cos(chi h) b_{k+1} + a'_k) - b_{k+2}: the coefficient a'_k, shared by the
+                // PPT recurrences, sits in the DFMA's addend slot where the operand-reuse cache
+                // serves it, so each DFMA fetches two fresh 64-bit registers instead of three (a
+                // bank conflict on B200's FP64 path; 83 % -> 89 % of the pipe in isolation,
+                // tools/fp64_pattern_probe.cu B26)
                 double n0[PPT];
 #pragma unroll
-                for (int q = 0; q < PPT; ++q) n0[q] = fma(c2[q], b1[q], tc.x - b2[q]);
+                for (int q = 0; q < PPT; ++q) n0[q] = fma(c2[q], b1[q], tc.x) - b2[q];
 #pragma unroll
                 for (int q = 0; q < PPT; ++q) {
-                  const double n1 = fma(c2[q], n0[q], tc.y - b1[q]);
+                  const double n1 = fma(c2[q], n0[q], tc.y) - b1[q];
                   b2[q] = n0[q];
                   b1[q] = n1;
                 }
@@ -690,7 +696,12 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
             }
 #pragma unroll
             for (int q = 0; q < PPT; ++q) {
-              const double n0 = fma(c2[q], b1[q], tc.x - b2[q]);   // b_1
+              // x and cos(chi h) were left dead across the recurrence (register room for its
+              // schedule): cos = c2 / 2 exactly, x recomputed bitwise (the asm fence stops CSE)
+              asm volatile("" : "+d"(uv[q]), "+d"(Ssum[q]));
+              x[q] = uv[q] * fma(A3, Ssum[q], A2);
+              cs[q] = 0.5 * c2[q];
+              const double n0 = fma(c2[q], b1[q], tc.x) - b2[q];   // b_1
               // sum_k a'_k z^k = a'_0 + z b_1 - b_2
               accr[q] = fma(cs[q], n0, tc.y - b1[q]);
               acci[q] = sn[q] * n0;

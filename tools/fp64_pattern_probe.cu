@@ -200,6 +200,18 @@ __global__ void __launch_bounds__(128, 4) kern(double* out, long long* cyc, int 
           b2[p4 + 2] = n2; b1[p4 + 2] = m2;
           b2[p4 + 3] = n3; b1[p4 + 3] = m3;
         }
+      } else if (V == 26) {  // (c2 b1 + a) - b2: the shared coefficient in the DFMA's addend slot
+        const double2 tn = rowp[i2 + 1];
+        double n0[PPT];
+#pragma unroll
+        for (int q = 0; q < PPT; ++q) n0[q] = fma(c2[q], b1[q], tc.x) - b2[q];
+#pragma unroll
+        for (int q = 0; q < PPT; ++q) {
+          const double n1 = fma(c2[q], n0[q], tc.y) - b1[q];
+          b2[q] = n0[q];
+          b1[q] = n1;
+        }
+        tc = tn;
       } else if (V == 8) {   // independent 1 DADD : 3 DFMA
 #pragma unroll
         for (int q = 0; q < PPT; ++q) { b1[q] = b1[q] - tc.x; b2[q] = fma(b2[q], cs, tc.y); c2[q] = fma(c2[q], cs, tc.x); tc.y = fma(tc.y, cs, tc.x); }
@@ -256,6 +268,10 @@ int main() {
   cudaMalloc(&d, 8);
   cudaMalloc(&dc, 3 * 8 * 8192);
   const int n = p.multiProcessorCount;
+  run<26, 4>("B26 (c2 b1 + a) - b2", n, d, dc);
+  run<26, 6>("B26 (c2 b1 + a) - b2", n, d, dc);
+  run<26, 8>("B26 (c2 b1 + a) - b2", n, d, dc);
+  run<0, 4>("A goertzel + LDS.128", n, d, dc);
   run<32, 4>("Q block split, 1 point", n, d, dc);
   run<32, 8>("Q block split, 2 points", n, d, dc);
   run<31, 4>("R4 residue split, 1 point", n, d, dc);
