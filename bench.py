@@ -62,7 +62,11 @@ def ncu_traffic():
     `ncu --set full` summary under profiles/ (tools/ncu_summary.py), or (None, None)."""
     import glob
     best = None
-    for fn in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_integrand*.json"))):
+    def order(fn):            # r01a < ... < r01z < r01aa < r01ab: by tag length, then name
+        tag = os.path.basename(fn).split("_")[0]
+        return (len(tag), tag)
+
+    for fn in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_integrand*.json")), key=order):
         if "fp32" in fn or "_c2" not in fn:   # the bench config's capture only
             continue
         try:
