@@ -1,5 +1,4 @@
-bash tools/gpu_run.sh r01ae f
-python tools/dz_sweep.py --config c2 --dz 500,1000,2000,4000 --ref 250 > gpurun_out/r01ae/dz_sweep_c2.jsonl 2>&1
-ISRS_EGN_LIB=build_variants/lib_prof.so python tools/ncu_target.py --config c2 --reps 2 > gpurun_out/r01ae/prof_c2.txt 2>&1
-grep ISRS_PROF gpurun_out/r01ae/prof_c2.txt | sort -u
-cut -c1-220 gpurun_out/r01ae/dz_sweep_c2.jsonl
+mkdir -p gpurun_out/r01af
+python tools/perf_variants.py build_variants/lib_*.so --reps=5 > gpurun_out/r01af/variants_c2.txt 2>&1
+python tools/perf_variants.py build_variants/lib_*.so --config=c5 --coi=100 --reps=1 > gpurun_out/r01af/variants_c5.txt 2>&1
+cat gpurun_out/r01af/variants_*.txt
