@@ -108,6 +108,21 @@ def test_degenerate_zero_gamma_and_empty_coi(isrs):
             e.nli(coi=[])
 
 
+def test_c_example_matches_oracle(isrs, tmp_path):
+    """examples/eta_c_abi.c (plain C, no Python/PyTorch) through the C ABI against the oracle on the
+    same 9-channel link it builds (16QAM, 3 x 80 km, N = 64)."""
+    import subprocess
+    from tests.test_abi import _compile_example
+    exe = _compile_example(str(tmp_path / "eta_c_abi"))
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    got = np.array([float(l.split()[3]) for l in r.stdout.splitlines() if l.startswith("channel")])
+    link = tiny_link(n_ch=9, rates_gbd=(64,), spacing_ghz=100.0, n_span=3, grid_n=64, fmts=("16qam",))
+    e_o, _ = egn.eta(link)
+    assert got.shape == e_o.shape
+    assert np.all(np.abs(got - e_o) / e_o <= TOL_ETA), np.abs(got - e_o) / e_o
+
+
 def test_eta_parity_c1_full(isrs):
     link = bj_config("c1")
     e_o, t_o = egn.eta(link)
