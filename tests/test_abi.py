@@ -129,22 +129,8 @@ def test_product_never_imports_oracle():
                 assert not re.search(r"^\s*(import|from)\s+paper_2412_11614_b200\b", txt, re.M), f
 
 
-def _compile_example(out):
-    import shutil
-    import subprocess
-    gcc = shutil.which("gcc")
-    if not gcc:
-        pytest.skip("no gcc")
-    lib = os.path.join(ROOT, "paper_2412_11614_b200")
-    cmd = [gcc, "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
-           os.path.join(ROOT, "examples", "eta_c_abi.c"), "-L", lib, "-lisrs_egn", "-L",
-           "/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath," + lib, "-lm", "-o", out]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    assert r.returncode == 0, r.stderr
-    return out
-
-
 def test_c_example_compiles_against_the_header_and_library(abi, tmp_path):
     """The boundary is usable from plain C: the example builds against include/isrs_egn.h and links
     libisrs_egn.so (it runs in tests/test_parity_gpu.py::test_c_example_matches_oracle)."""
-    _compile_example(str(tmp_path / "eta_c_abi"))
+    from _helpers import compile_c_example
+    compile_c_example(str(tmp_path / "eta_c_abi"))

@@ -112,8 +112,8 @@ def test_c_example_matches_oracle(isrs, tmp_path):
     """examples/eta_c_abi.c (plain C, no Python/PyTorch) through the C ABI against the oracle on the
     same 9-channel link it builds (16QAM, 3 x 80 km, N = 64)."""
     import subprocess
-    from tests.test_abi import _compile_example
-    exe = _compile_example(str(tmp_path / "eta_c_abi"))
+    from _helpers import compile_c_example
+    exe = compile_c_example(str(tmp_path / "eta_c_abi"))
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr
     got = np.array([float(l.split()[3]) for l in r.stdout.splitlines() if l.startswith("channel")])
@@ -334,6 +334,16 @@ def test_integral_form_parity_tiny(isrs, name):
     e_o, _ = egn.eta(link, mu_mode="quad")
     e_g, _ = gpu_eta(isrs, link, mu_mode=isrs.MU_INTEGRAL)
     assert np.all(np.abs(e_g - e_o) / e_o <= TOL_ETA), (name, np.abs(e_g - e_o) / e_o)
+
+
+def test_integral_form_vs_segment_c1_all_cois(isrs):
+    """Pin P4 on BASELINE configs[0]: the segment closed form (dz = 1 km) within 0.001 dB MAE of the
+    integral form (Eq. 23) for every COI of c1."""
+    link = bj_config("c1")
+    quad, _ = gpu_eta(isrs, link, mu_mode=isrs.MU_INTEGRAL)
+    seg, _ = gpu_eta(isrs, link)
+    err = np.abs(10 * np.log10(seg) - 10 * np.log10(quad))
+    assert err.mean() < 1e-3 and err.max() < 2.7e-3, err
 
 
 def test_integral_form_vs_segment_pa_ir(isrs):
