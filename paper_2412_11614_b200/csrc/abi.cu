@@ -558,6 +558,10 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
   ce = cudaGetLastError();
   if (ce != cudaSuccess) return cuda_fail(ce, "pending CUDA error");
   if (!(h->have_result || h->wl.desc.size()) || h->wl.coi != c) {
+    // region ids are int32 and the f-sample index lives in 23 flag bits
+    const double nreg_max = (double)c.size() * std::max(1, h->num.f_samples) * h->n_ch * h->n_ch;
+    if (nreg_max > 2147483647.0 || (double)c.size() * std::max(1, h->num.f_samples) >= 8388608.0)
+      return fail(ISRS_EGN_ERANGE, "n_coi x f_samples x n_ch^2 regions exceed the 2^31 work-list limit");
     // (re)build and upload the work list for this COI set (cached across identical calls)
     cudaStreamSynchronize(h->last_stream);
     build_worklist(h, c, &h->wl);
