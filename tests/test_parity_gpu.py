@@ -148,6 +148,17 @@ def test_unit_link_hook_matches_closed_form(isrs):
         assert abs(e_g[0] - egn.unit_link_eta(phi, psi)) < 2e-5
 
 
+def test_unit_link_maximum_grid_N4096(isrs):
+    """Maximum grid (grid_n = 4096: 16.7 M points, 8191 lattice lines in 16 line segments, the
+    coherent kernel's 64 KB row/column accumulators): with Y := 1 the D and H integrals are exact at
+    every even N (pin P6), so the CUDA path must return 4/9 and Psi/9 to rounding."""
+    link = tiny_link(n_ch=1, rates_gbd=(64,), n_span=1, grid_n=4096, fmts=("qpsk",))
+    e_g, t_g = gpu_eta(isrs, link, flags=isrs.FLAG_UNIT_LINK)
+    assert abs(t_g[0, 0] - 4.0 / 9.0) < 1e-12
+    assert abs(t_g[0, 4] - 4.0 / 9.0) < 1e-12                   # Psi(QPSK) / 9 = 4/9
+    assert abs(e_g[0] - egn.unit_link_eta(-1.0, 4.0)) < 1e-6    # E, F, G at O(h^2), h = R/4096
+
+
 def test_maclaurin_mode_parity(isrs):
     link = tiny_link(**TINY["three_islands_96gbd"])
     e_o, _ = egn.eta(link, mu_mode="maclaurin")
