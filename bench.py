@@ -316,6 +316,7 @@ def run_ours(args, link, ws, rank, local):
     peak = fp64_peak_tflops()
     slots_ach = ps_i * spp / (ki_ms * 1e-3) / 1e12
     traffic, traffic_src = ncu_traffic()
+    survey_fpp = float(np.mean(8 * np.asarray(k_s, dtype=float) + 100))     # 8 K_s + ~100
     slots_peak = SMS * FP64_LANES * SM_MAX_MHZ * 1e6 / 1e12
 
     # end to end through the public API with host buffers: create + nli + D2H + destroy
@@ -388,6 +389,13 @@ def run_ours(args, link, ws, rank, local):
                              "span_chains": [int(g) for g in chain_g],
                              "peak_note": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz "
                                           "(tools/dmma_probe.cu: a DFMA stream reaches 128 flop/SM-cycle = this peak)"},
+                "survey_units": {"flops_per_point_span": survey_fpp,
+                                 "achieved": ps_i * survey_fpp / (ki_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                                 "frac": ps_i * survey_fpp / (ki_ms * 1e-3) / 1e12 / peak,
+                                 "note": "SURVEY.md 8(d) per-unit figure 8 K + 100 assumes a complex Horner "
+                                         "step (8 flops per segment); this kernel's real second-order "
+                                         "recurrence needs 3, so this ratio exceeds 1 and is not the "
+                                         "roofline - `roofline` counts the flops the kernel's method needs"},
                 "fp64_pipe_slots": {"achieved": slots_ach, "peak": slots_peak, "unit": "T slot/s",
                                     "frac": slots_ach / slots_peak, "per_point_span": spp,
                                     "note": "same algorithmic count with DFMA and DADD one FP64 "
