@@ -313,7 +313,9 @@ def run_ours(args, link, ws, rank, local):
     chain_g, k_s = eng.span_chains()
     fpp, spp = (v / link.n_span for v in algorithmic_work_per_point(chain_g, k_s))  # per point-span
     ach = ps_i * fpp / (ki_ms * 1e-3) / 1e12
-    peak = fp64_peak_tflops()
+    # fp64: 64 FP64 FMA lanes per SM; the mixed fp32 variant (a8) runs its recurrence on the
+    # 128 FP32 FMA lanes per SM, so its roofline takes the FP32 peak (2x)
+    peak = fp64_peak_tflops() * (2.0 if args.precision == 32 else 1.0)
     slots_ach = ps_i * spp / (ki_ms * 1e-3) / 1e12
     traffic, traffic_src = ncu_traffic()
     survey_fpp = float(np.mean(8 * np.asarray(k_s, dtype=float) + 100))     # 8 K_s + ~100
@@ -387,8 +389,11 @@ def run_ours(args, link, ws, rank, local):
                                        "regions, concurrent; fork to join)",
                              "flops_per_point_span": fpp,
                              "span_chains": [int(g) for g in chain_g],
-                             "peak_note": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz "
-                                          "(tools/dmma_probe.cu: a DFMA stream reaches 128 flop/SM-cycle = this peak)"},
+                             "peak_note": ("derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz "
+                                           "(tools/dmma_probe.cu: a DFMA stream reaches 128 flop/SM-cycle = this peak)"
+                                           if args.precision == 64 else
+                                           "derived FP32 peak: 148 SM x 128 FP32 FMA/clk x 2 x 1965 MHz (the "
+                                           "variant's recurrence is fp32; chi h, phase and Y stay fp64)")},
                 "survey_units": {"flops_per_point_span": survey_fpp,
                                  "achieved": ps_i * survey_fpp / (ki_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                                  "frac": ps_i * survey_fpp / (ki_ms * 1e-3) / 1e12 / peak,
