@@ -19,9 +19,10 @@ Modules
   formats  — Phi, Psi from constellation moments (reading C9)
   isrs     — L_eff, zeta, rho(z,f) Eq. 13/25, SRS gain Eq. 14, Delta-rho Eq. 12
   fwm      — chi Eq. 5, GN eta Eq. 6, segment mu Eqs. 8-10, Maclaurin mu Eq. 4, quad mu Eq. 23
-  link     — link function Y, Eq. 22 (reading C3)
+  link     — link function Y, Eq. 22 (reading C3; the literal gain products, NEXT-4b / R11)
   egn      — canonicalisation (C5), regions/islands (Eq. 16 generalised), grid (C6),
-             gates (C10), island terms D..H (Eqs. 17-21, C7), eta assembly (Eqs. 11, 15, C2)
+             gates (C10), island terms D..H (Eqs. 17-21, C7), eta assembly (Eqs. 11, 15, C2),
+             the 3-D form over the COI band (NEXT-3 / R10)
 
 Parity status: every function is pinned by a `-m "not gpu"` test in tests/test_oracle_*.py
 except where its docstring says "parity unpinned" (DESIGN.md lists those).
