@@ -293,6 +293,334 @@ __device__ inline long long gcd_ll(long long a, long long b) {
   return a;
 }
 
+// Line scan of lines [seg0, seg0 + nl) of a region (rows a3 of SURVEY §8): on each lattice line
+// j = a m1 + b m2 the f3 = C + g j is constant (exact), so the point count, the first m1 and the
+// C10 gate weights (line_gate) are per line; supported lines are compacted in order into sm.sl_*
+// with their slot offsets (each line padded to whole PPT-groups).  Returns (lines, slots, points).
+// All threads must call (block scan).
+__device__ __forceinline__ int4 scan_lines(const KParams& p, const Smem& sm, int seg0, int nl, int N, int a,
+                                           int b, int inv_a, int k1, int k2, double C, double g) {
+  const int tid = threadIdx.x;
+  // ---- line scan: each thread owns LPT consecutive lines (order-preserving compaction)
+  int cnt[LPT], first[LPT];
+  double lwD[LPT], lwE[LPT], lwF[LPT];
+  int4 v = make_int4(0, 0, 0, 0);
+#pragma unroll
+  for (int q = 0; q < LPT; ++q) {
+    const int jl = LPT * tid + q;
+    cnt[q] = 0;
+    first[q] = 0;
+    lwD[q] = lwE[q] = lwF[q] = 0.0;
+    if (jl < nl) {
+      const int j = seg0 + jl;
+      // points on the line: a m1 + b m2 = j, 0 <= m1, m2 < N
+      int lowb = j - b * (N - 1);
+      lowb = (lowb <= 0) ? 0 : (lowb + a - 1) / a;
+      const int upb = min(N - 1, j / a);
+      int fm = lowb;
+      if (b > 1) {
+        const int r = (int)(((long long)(j % b) * inv_a) % b);
+        fm = lowb + (((r - lowb) % b) + b) % b;
+      }
+      const int n = (fm <= upb) ? (upb - fm) / b + 1 : 0;
+      if (n > 0) {
+        const double f3 = __dadd_rn(C, g * (double)j);
+        line_gate(p, f3, k1, k2, &lwD[q], &lwE[q], &lwF[q]);
+        if (lwD[q] > 0.0) {
+          cnt[q] = n;
+          first[q] = fm;
+          v.x += 1;
+          v.y += (n + PPT - 1) / PPT * PPT;   // slots: each line padded to whole PPT-groups
+          v.z += n;
+        }
+      }
+    }
+  }
+  int4 tot;
+  int4 pos = block_scan3(v, sm.scan, &tot);
+#pragma unroll
+  for (int q = 0; q < LPT; ++q) {
+    if (cnt[q] > 0) {
+      sm.sl_j[pos.x] = seg0 + LPT * tid + q;
+      sm.sl_first[pos.x] = first[q];
+      sm.sl_start[pos.x] = pos.y;
+      sm.sl_cnt[pos.x] = cnt[q];
+      sm.wD[pos.x] = lwD[q];
+      sm.wE[pos.x] = lwE[q];
+      sm.wF[pos.x] = lwF[q];
+      pos.x += 1;
+      pos.y += (cnt[q] + PPT - 1) / PPT * PPT;
+    }
+  }
+  return tot;
+}
+
+// Envelope table (row a2 values at this region's lines): rows [tb, tb + tn) of the compacted
+// lines, row r holding a'_k(f3(j_r)) = c_k e^{-zeta_k f3} e^{-alpha h k} for k = Kp-1 .. 0 (reversed
+// for the recurrence), fp64 with the first pair repeated at the end (chain wrap, R9) or fp32 (a8).
+template <bool F32>
+__device__ __forceinline__ void build_table(const KParams& p, const Smem& sm, int cls, int tb, int tn, double C,
+                                            double g) {
+  const int tid = threadIdx.x;
+  const int Kc = __ldg(p.Kc + cls);
+  // fp64 rows: K rounded up to even (16-byte pair loads); fp32 rows (a8): to a
+  // multiple of 4 (float4 loads), row stride 2 tstride floats
+  const int Kp = F32 ? ((Kc + 3) & ~3) : ((Kc + 1) & ~1);
+  float* T32 = reinterpret_cast<float*>(sm.T);
+  const double* lnA = p.lnA + (size_t)cls * p.kstride;
+  const double* zt = p.zeta + (size_t)cls * p.kstride;
+  // one thread per coefficient k walks the rows: a'_k(f3 + g) = a'_k(f3) e^{-zeta_k g}
+  // (one DMUL per entry; rows whose line index jumps restart from exp; <= tw steps,
+  // relative error <= tw eps)
+  for (int ii = tid; ii < Kp; ii += BLOCK) {
+    const int k = Kp - 1 - ii;
+    const bool live = k < Kc;
+    const double la = live ? __ldg(lnA + k) : 0.0, ze = live ? __ldg(zt + k) : 0.0;
+    const double step = exp(-ze * g);
+    double v = 0.0;
+    int jprev = -2;
+    for (int row = 0; row < tn; ++row) {
+      const int j = sm.sl_j[tb + row];
+      if (live) v = (j == jprev + 1) ? v * step : exp(la - ze * __dadd_rn(C, g * (double)j));
+      jprev = j;
+      if (F32) {
+        T32[row * 2 * p.tstride + ii] = (float)v;
+      } else {
+        sm.T[row * p.tstride + ii] = v;
+        if (ii < 2) sm.T[row * p.tstride + Kp + ii] = v;   // wrap pair for span chains (R9)
+      }
+    }
+  }
+}
+
+// Coherent sums of one chunk (reading C7; Eqs. 18-21), the chunk's Y values staged in sm.ybuf:
+// line sums (G, H) by one thread per line, row sums r[m2] (E) and column sums c[m1] (F) by one
+// thread per row / column, each accumulated over the chunk's lines in line order (deterministic).
+__device__ __forceinline__ void coherent_chunk(const Smem& sm, int flags, int N, int a, int b, int i_first,
+                                               int i_last, int p0, int p_end) {
+  const int tid = threadIdx.x;
+  // lines (G, H): one thread per line in the chunk, points in order
+  if (flags & (NEED_G | NEED_H)) {
+    for (int i = i_first + tid; i <= i_last; i += BLOCK) {
+      const int s0 = max(sm.sl_start[i], p0), s1 = min(sm.sl_start[i] + sm.sl_cnt[i], p_end);
+      double2 acc = sm.lineacc[i];
+      for (int t = s0; t < s1; ++t) {
+        const double2 y = sm.ybuf[t - p0];
+        acc.x += y.x;
+        acc.y += y.y;
+      }
+      sm.lineacc[i] = acc;
+    }
+  }
+  // rows (E): r[m2] += sum over the chunk's lines of wE Y(m1, m2), line order
+  if (flags & NEED_E) {
+    for (int m2 = tid; m2 < N; m2 += BLOCK) {
+      double2 acc = sm.rowacc[m2];
+      for (int i = i_first; i <= i_last; ++i) {
+        const double w = sm.wE[i];
+        if (w == 0.0) continue;
+        const int num = sm.sl_j[i] - b * m2;
+        if (num < 0 || num % a) continue;
+        const int m1 = num / a;
+        if (m1 >= N) continue;
+        const int idx = sm.sl_start[i] + (m1 - sm.sl_first[i]) / b;
+        if (m1 < sm.sl_first[i] || idx < p0 || idx >= p_end) continue;
+        const double2 y = sm.ybuf[idx - p0];
+        acc.x = fma(w, y.x, acc.x);
+        acc.y = fma(w, y.y, acc.y);
+      }
+      sm.rowacc[m2] = acc;
+    }
+  }
+  // columns (F): c[m1] += sum over the chunk's lines of wF Y(m1, m2)
+  if (flags & NEED_F) {
+    for (int m1 = tid; m1 < N; m1 += BLOCK) {
+      double2 acc = sm.colacc[m1];
+      for (int i = i_first; i <= i_last; ++i) {
+        const double w = sm.wF[i];
+        if (w == 0.0) continue;
+        const int num = sm.sl_j[i] - a * m1;
+        if (num < 0 || num % b) continue;
+        const int m2 = num / b;
+        if (m2 >= N || m1 < sm.sl_first[i]) continue;
+        const int idx = sm.sl_start[i] + (m1 - sm.sl_first[i]) / b;
+        if (idx < p0 || idx >= p_end) continue;
+        const double2 y = sm.ybuf[idx - p0];
+        acc.x = fma(w, y.x, acc.x);
+        acc.y = fma(w, y.y, acc.y);
+      }
+      sm.colacc[m1] = acc;
+    }
+  }
+}
+
+// NEXT-1: the Maclaurin closed form (Eq. 4) of one span for one point, times gamma:
+//   mu = eta - (P C f3 / alpha)(eta - eta2),  eta = (e^{(i chi - alpha)L} - 1)/(i chi - alpha),
+//   eta2 the same with 2 alpha; x = chi h / pi, px = chi h, ah = alpha h, gh = gamma h.
+__device__ __forceinline__ void mu_maclaurin(const KParams& p, int s, double x, double px, double ah, double gh,
+                                             int Ks, double f3l, double* mr, double* mi) {
+  const double aL = __ldg(p.aL + s);
+  double sl, cl;
+  sincospi_d(x * Ks, &sl, &cl);                  // e^{i chi L}
+  const double e1 = exp(-aL), e2 = e1 * e1;
+  // eta / h = (e1 cis(chi L) - 1) / ((i chi - alpha) h): multiply by conj(d) / |d|^2
+  const double ar = -ah, ai = px;                // d = (i chi - alpha) h
+  const double den1 = 1.0 / fma(ai, ai, ar * ar);
+  const double n1r = fma(e1, cl, -1.0), n1i = e1 * sl;
+  const double eta_r = (n1r * ar + n1i * ai) * den1;
+  const double eta_i = (n1i * ar - n1r * ai) * den1;
+  const double br = -2.0 * ah;
+  const double den2 = 1.0 / fma(ai, ai, br * br);
+  const double n2r = fma(e2, cl, -1.0), n2i = e2 * sl;
+  const double et2_r = (n2r * br + n2i * ai) * den2;
+  const double et2_i = (n2i * br - n2r * ai) * den2;
+  const double cf = __ldg(p.mac_c + s) * f3l;
+  // (values above are eta / h; gh = gamma h restores the scale)
+  *mr = (eta_r - cf * (eta_r - et2_r)) * gh;
+  *mi = (eta_i - cf * (eta_i - et2_i)) * gh;
+}
+
+// ---- NEXT-2: one span of the integral form for the thread's PPT points (MODE_QUAD)
+__device__ __forceinline__ void span_quad(const KParams& p, int s, int ch, double A2, double A3, int Ks,
+                                          double f3l, const double (&uv)[PPT], const double (&Ssum)[PPT],
+                                          const bool (&valid)[PPT], double (&yr)[PPT], double (&yi)[PPT],
+                                          double (&th)[PPT]) {
+  // ---- NEXT-2: Eq. 23 mu_s = int_0^L rho_s(z, f3) e^{i chi z} dz by the oracle's rule
+  // (reading C12): n = max(64, 4|chi|L/2pi) equal panels rounded up to 2^k, 12-node
+  // Gauss-Legendre each; rho_s from Eq. 25 evaluated at every node (the paper's slow
+  // baseline: cost grows with the oscillation |chi| L).  Points run one at a time.
+  const double Lsp = __ldg(p.Ls + s), al = __ldg(p.alpha + s), gam = __ldg(p.gamma + s);
+  const double pcr = __ldg(p.pcr + s);
+  for (int q = 0; q < PPT; ++q) {
+    const double xq = uv[q] * fma(A3, Ssum[q], A2);       // chi h / pi
+    const double xk = xq * Ks;                            // chi L / pi
+    double mr = 0.0, mi = 0.0;
+    if (valid[q]) {
+      const double want = fmax(64.0, ceil(2.0 * fabs(xk)));   // 4 |chi| L / (2 pi)
+      long long npan = 64;
+      while ((double)npan < want) npan <<= 1;
+      const double hp = Lsp / (double)npan, hh = 0.5 * hp;
+      const double xz = xk / Lsp;                         // chi / pi per metre
+      for (long long j = 0; j < npan; ++j) {
+        const double z0 = (double)j * hp;
+#pragma unroll
+        for (int gq = 0; gq < 12; ++gq) {
+          const double z = fma(p.gl_x[gq] + 1.0, hh, z0);
+          const double ze = pcr * (-expm1(-al * z)) / al;          // Eq. 2: zeta(z)
+          const double xx = p.b_tot * ze;
+          // Eq. 25: B P C L_eff e^{-alpha z - zeta f3} / (2 sinh(x/2)), x = B zeta
+          const double c = (xx == 0.0) ? 1.0 : xx / (-expm1(-xx));
+          const double rho = c * exp(-0.5 * xx - ze * f3l - al * z);
+          double sz, cz;
+          sincospi_d(xz * z, &sz, &cz);                  // e^{i chi z} (Eq. 24)
+          const double wr = p.gl_w[gq] * rho;
+          mr = fma(wr, cz, mr);
+          mi = fma(wr, sz, mi);
+        }
+      }
+      mr *= hh * gam;
+      mi *= hh * gam;
+    }
+    double ps = 0.0, pc = 1.0;
+    if (ch > 0) sincospi_d(th[q], &ps, &pc);
+    yr[q] = fma(mr, pc, fma(-mi, ps, yr[q]));
+    yi[q] = fma(mr, ps, fma(mi, pc, yi[q]));
+    const double t2 = fma(xq, (double)Ks, th[q]);
+    th[q] = t2 - 2.0 * rint(0.5 * t2);
+  }
+}
+
+// ---- row a8: one run of G identical spans in the mixed fp32 variant (MODE_SEG32); rowf is the
+// thread's fp32 envelope-table row
+__device__ __forceinline__ void span_seg32(const KParams& p, int ch, int G, int cls, double A2, double A3,
+                                           double Eh, double ah, double gh, int Ks, const float* rowf,
+                                           const double (&uv)[PPT], const double (&Ssum)[PPT],
+                                           double (&yr)[PPT], double (&yi)[PPT], double (&th)[PPT]) {
+  // ---- row a8: mixed fp32 variant (no span chains).  chi h / pi and its reduction
+  // mod 2 stay fp64 (exact); z = cis(pi r) by sincospif; the recurrence runs on pairs
+  // of points with packed FFMA2; I_0, mu and the span phase factor in fp32; the phase
+  // advance and Y accumulate in fp64.
+  const float Ehf = (float)Eh, ahf = (float)ah, ghf = (float)gh;
+  const int Kp4 = (__ldg(p.Kc + cls) + 3) & ~3;
+  const float4* rowq = reinterpret_cast<const float4*>(rowf);
+  double xs[PPT];
+  float sf[PPT], cf[PPT], nrf[PPT], nif[PPT], prr[PPT], pri[PPT], drr[PPT], dri[PPT];
+  float2 c2[PPT / 2];
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    xs[q] = uv[q] * fma(A3, Ssum[q], A2);                 // chi h / pi
+    const double r = xs[q] - 2.0 * rint(0.5 * xs[q]);     // exact, |r| <= 1
+    sincospif((float)r, &sf[q], &cf[q]);
+    // I_0 = (w - 1)/(i chi - alpha): the same for every span of the run (G identical spans)
+    const float px = (float)(CUDART_PI * xs[q]);
+    const float wr1 = fmaf(Ehf, cf[q], -1.f), wi = Ehf * sf[q];
+    const float inv = __fdividef(ghf, fmaf(px, px, ahf * ahf));
+    nrf[q] = fmaf(wi, px, -ahf * wr1) * inv;
+    nif[q] = -fmaf(px, wr1, ahf * wi) * inv;
+    // span phase e^{i theta_s} and its per-span step e^{i chi L} (reading C3)
+    const double tk = xs[q] * Ks;
+    const double rk = tk - 2.0 * rint(0.5 * tk);
+    sincospif((float)rk, &dri[q], &drr[q]);
+    if (ch > 0) __sincosf(CUDART_PI_F * (float)th[q], &pri[q], &prr[q]);
+    else { pri[q] = 0.f; prr[q] = 1.f; }
+  }
+#pragma unroll
+  for (int hq = 0; hq < PPT / 2; ++hq) c2[hq] = make_float2(2.f * cf[2 * hq], 2.f * cf[2 * hq + 1]);
+  const float2 neg1 = make_float2(-1.f, -1.f);
+  const int n4 = Kp4 >> 2;
+  for (int gi = 0; gi < G; ++gi) {
+    // ---- each span's own K-segment recurrence (Eqs. 8-9)
+    float2 b1[PPT / 2], b2[PPT / 2];
+#pragma unroll
+    for (int hq = 0; hq < PPT / 2; ++hq) {
+      b1[hq] = make_float2(0.f, 0.f);
+      b2[hq] = make_float2(0.f, 0.f);
+    }
+    auto step = [&](float a) {
+#pragma unroll
+      for (int hq = 0; hq < PPT / 2; ++hq) {
+        // (2cos b_{k+1} + a) - b_{k+2}: the shared a in the addend slot (operand reuse)
+        const float2 t = __ffma2_rn(c2[hq], b1[hq], make_float2(a, a));
+        const float2 n = __ffma2_rn(b2[hq], neg1, t);
+        b2[hq] = b1[hq];
+        b1[hq] = n;
+      }
+    };
+    float4 tc = rowq[0];
+#pragma unroll 2
+    for (int i4 = 0; i4 < n4 - 1; ++i4) {
+      const float4 tn = rowq[i4 + 1];
+      step(tc.x);
+      step(tc.y);
+      step(tc.z);
+      step(tc.w);
+      tc = tn;
+    }
+    step(tc.x);
+    step(tc.y);
+    step(tc.z);                                           // -> b_1, b_2
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const float bb1 = (q & 1) ? b1[q >> 1].y : b1[q >> 1].x;
+      const float bb2 = (q & 1) ? b2[q >> 1].y : b2[q >> 1].x;
+      const float accr = fmaf(cf[q], bb1, tc.w - bb2);     // a'_0 + z b_1 - b_2
+      const float acci = sf[q] * bb1;
+      const float mr = nrf[q] * accr - nif[q] * acci;      // mu_s = I_0 sum
+      const float mi = nrf[q] * acci + nif[q] * accr;
+      yr[q] += (double)fmaf(mr, prr[q], -mi * pri[q]);     // Y += gamma mu e^{i theta_s}
+      yi[q] += (double)fmaf(mr, pri[q], mi * prr[q]);
+      const float npr = fmaf(prr[q], drr[q], -pri[q] * dri[q]);
+      pri[q] = fmaf(prr[q], dri[q], pri[q] * drr[q]);
+      prr[q] = npr;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const double t2 = fma(xs[q], (double)(Ks * G), th[q]);
+    th[q] = t2 - 2.0 * rint(0.5 * t2);
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // integrand (rows a3-a6)
 
@@ -342,57 +670,8 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
   PROF_MARK(0)   // prologue
   for (int seg0 = 0; seg0 < J; seg0 += LINE_CAP) {
     const int nl = min(LINE_CAP, J - seg0);
-    // ---- line scan: each thread owns LPT consecutive lines (order-preserving compaction)
-    int cnt[LPT], first[LPT];
-    double lwD[LPT], lwE[LPT], lwF[LPT];
-    int4 v = make_int4(0, 0, 0, 0);
-#pragma unroll
-    for (int q = 0; q < LPT; ++q) {
-      const int jl = LPT * tid + q;
-      cnt[q] = 0;
-      first[q] = 0;
-      lwD[q] = lwE[q] = lwF[q] = 0.0;
-      if (jl < nl) {
-        const int j = seg0 + jl;
-        // points on the line: a m1 + b m2 = j, 0 <= m1, m2 < N
-        int lowb = j - b * (N - 1);
-        lowb = (lowb <= 0) ? 0 : (lowb + a - 1) / a;
-        const int upb = min(N - 1, j / a);
-        int fm = lowb;
-        if (b > 1) {
-          const int r = (int)(((long long)(j % b) * inv_a) % b);
-          fm = lowb + (((r - lowb) % b) + b) % b;
-        }
-        const int n = (fm <= upb) ? (upb - fm) / b + 1 : 0;
-        if (n > 0) {
-          const double f3 = __dadd_rn(C, g * (double)j);
-          line_gate(p, f3, k1, k2, &lwD[q], &lwE[q], &lwF[q]);
-          if (lwD[q] > 0.0) {
-            cnt[q] = n;
-            first[q] = fm;
-            v.x += 1;
-            v.y += (n + PPT - 1) / PPT * PPT;   // slots: each line padded to whole PPT-groups
-            v.z += n;
-          }
-        }
-      }
-    }
-    int4 tot;
-    int4 pos = block_scan3(v, sm.scan, &tot);
-#pragma unroll
-    for (int q = 0; q < LPT; ++q) {
-      if (cnt[q] > 0) {
-        sm.sl_j[pos.x] = seg0 + LPT * tid + q;
-        sm.sl_first[pos.x] = first[q];
-        sm.sl_start[pos.x] = pos.y;
-        sm.sl_cnt[pos.x] = cnt[q];
-        sm.wD[pos.x] = lwD[q];
-        sm.wE[pos.x] = lwE[q];
-        sm.wF[pos.x] = lwF[q];
-        pos.x += 1;
-        pos.y += (cnt[q] + PPT - 1) / PPT * PPT;
-      }
-    }
+    // ---- line scan (gates, point counts) and order-preserving compaction of supported lines
+    const int4 tot = scan_lines(p, sm, seg0, nl, N, a, b, inv_a, k1, k2, C, g);
     const int S = tot.x, NP = tot.y;
     if (tid == 0) sm.sl_start[S] = NP;
     if (COH) {
@@ -467,35 +746,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
             tb = i_first;
             tn = (p.n_cls == 1) ? min(p.tw, S - i_first) : (i_last - i_first + 1);
             tcls = cls;
-            const int Kc = __ldg(p.Kc + cls);
-            // fp64 rows: K rounded up to even (16-byte pair loads); fp32 rows (a8): to a
-            // multiple of 4 (float4 loads), row stride 2 tstride floats
-            const int Kp = (MODE == MODE_SEG32) ? ((Kc + 3) & ~3) : ((Kc + 1) & ~1);
-            float* T32 = reinterpret_cast<float*>(sm.T);
-            const double* lnA = p.lnA + (size_t)cls * p.kstride;
-            const double* zt = p.zeta + (size_t)cls * p.kstride;
-            // one thread per coefficient k walks the rows: a'_k(f3 + g) = a'_k(f3) e^{-zeta_k g}
-            // (one DMUL per entry; rows whose line index jumps restart from exp; <= tw steps,
-            // relative error <= tw eps)
-            for (int ii = tid; ii < Kp; ii += BLOCK) {
-              const int k = Kp - 1 - ii;
-              const bool live = k < Kc;
-              const double la = live ? __ldg(lnA + k) : 0.0, ze = live ? __ldg(zt + k) : 0.0;
-              const double step = exp(-ze * g);
-              double v = 0.0;
-              int jprev = -2;
-              for (int row = 0; row < tn; ++row) {
-                const int j = sm.sl_j[tb + row];
-                if (live) v = (j == jprev + 1) ? v * step : exp(la - ze * __dadd_rn(C, g * (double)j));
-                jprev = j;
-                if (MODE == MODE_SEG32) {
-                  T32[row * 2 * p.tstride + ii] = (float)v;
-                } else {
-                  sm.T[row * p.tstride + ii] = v;
-                  if (ii < 2) sm.T[row * p.tstride + Kp + ii] = v;   // wrap pair for span chains (R9)
-                }
-              }
-            }
+            build_table<MODE == MODE_SEG32>(p, sm, cls, tb, tn, C, g);
             __syncthreads();
           }
           PROF_MARK(3)   // table (re)build incl. barriers
@@ -504,136 +755,13 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
           const double Eh = __ldg(p.Eh + s), ah = __ldg(p.ah + s), gh = __ldg(p.gh + s);
           const int Ks = __ldg(p.K + s);
           if (MODE == MODE_QUAD) {
-            // ---- NEXT-2: Eq. 23 mu_s = int_0^L rho_s(z, f3) e^{i chi z} dz by the oracle's rule
-            // (reading C12): n = max(64, 4|chi|L/2pi) equal panels rounded up to 2^k, 12-node
-            // Gauss-Legendre each; rho_s from Eq. 25 evaluated at every node (the paper's slow
-            // baseline: cost grows with the oscillation |chi| L).  Points run one at a time.
-            const double Lsp = __ldg(p.Ls + s), al = __ldg(p.alpha + s), gam = __ldg(p.gamma + s);
-            const double pcr = __ldg(p.pcr + s);
-            for (int q = 0; q < PPT; ++q) {
-              const double xq = uv[q] * fma(A3, Ssum[q], A2);       // chi h / pi
-              const double xk = xq * Ks;                            // chi L / pi
-              double mr = 0.0, mi = 0.0;
-              if (valid[q]) {
-                const double want = fmax(64.0, ceil(2.0 * fabs(xk)));   // 4 |chi| L / (2 pi)
-                long long npan = 64;
-                while ((double)npan < want) npan <<= 1;
-                const double hp = Lsp / (double)npan, hh = 0.5 * hp;
-                const double xz = xk / Lsp;                         // chi / pi per metre
-                for (long long j = 0; j < npan; ++j) {
-                  const double z0 = (double)j * hp;
-#pragma unroll
-                  for (int gq = 0; gq < 12; ++gq) {
-                    const double z = fma(p.gl_x[gq] + 1.0, hh, z0);
-                    const double ze = pcr * (-expm1(-al * z)) / al;          // Eq. 2: zeta(z)
-                    const double xx = p.b_tot * ze;
-                    // Eq. 25: B P C L_eff e^{-alpha z - zeta f3} / (2 sinh(x/2)), x = B zeta
-                    const double c = (xx == 0.0) ? 1.0 : xx / (-expm1(-xx));
-                    const double rho = c * exp(-0.5 * xx - ze * f3l - al * z);
-                    double sz, cz;
-                    sincospi_d(xz * z, &sz, &cz);                  // e^{i chi z} (Eq. 24)
-                    const double wr = p.gl_w[gq] * rho;
-                    mr = fma(wr, cz, mr);
-                    mi = fma(wr, sz, mi);
-                  }
-                }
-                mr *= hh * gam;
-                mi *= hh * gam;
-              }
-              double ps = 0.0, pc = 1.0;
-              if (ch > 0) sincospi_d(th[q], &ps, &pc);
-              yr[q] = fma(mr, pc, fma(-mi, ps, yr[q]));
-              yi[q] = fma(mr, ps, fma(mi, pc, yi[q]));
-              const double t2 = fma(xq, (double)Ks, th[q]);
-              th[q] = t2 - 2.0 * rint(0.5 * t2);
-            }
+            span_quad(p, s, ch, A2, A3, Ks, f3l, uv, Ssum, valid, yr, yi, th);
             continue;
           }
           if (MODE == MODE_SEG32) {
-            // ---- row a8: mixed fp32 variant (no span chains).  chi h / pi and its reduction
-            // mod 2 stay fp64 (exact); z = cis(pi r) by sincospif; the recurrence runs on pairs
-            // of points with packed FFMA2; I_0, mu and the span phase factor in fp32; the phase
-            // advance and Y accumulate in fp64.
-            const float Ehf = (float)Eh, ahf = (float)ah, ghf = (float)gh;
-            const int Kp4 = (__ldg(p.Kc + cls) + 3) & ~3;
-            const float4* rowq =
-                reinterpret_cast<const float4*>(reinterpret_cast<const float*>(sm.T) + (li - tb) * 2 * p.tstride);
-            double xs[PPT];
-            float sf[PPT], cf[PPT], nrf[PPT], nif[PPT], prr[PPT], pri[PPT], drr[PPT], dri[PPT];
-            float2 c2[PPT / 2];
-#pragma unroll
-            for (int q = 0; q < PPT; ++q) {
-              xs[q] = uv[q] * fma(A3, Ssum[q], A2);                 // chi h / pi
-              const double r = xs[q] - 2.0 * rint(0.5 * xs[q]);     // exact, |r| <= 1
-              sincospif((float)r, &sf[q], &cf[q]);
-              // I_0 = (w - 1)/(i chi - alpha): the same for every span of the run (G identical spans)
-              const float px = (float)(CUDART_PI * xs[q]);
-              const float wr1 = fmaf(Ehf, cf[q], -1.f), wi = Ehf * sf[q];
-              const float inv = __fdividef(ghf, fmaf(px, px, ahf * ahf));
-              nrf[q] = fmaf(wi, px, -ahf * wr1) * inv;
-              nif[q] = -fmaf(px, wr1, ahf * wi) * inv;
-              // span phase e^{i theta_s} and its per-span step e^{i chi L} (reading C3)
-              const double tk = xs[q] * Ks;
-              const double rk = tk - 2.0 * rint(0.5 * tk);
-              sincospif((float)rk, &dri[q], &drr[q]);
-              if (ch > 0) __sincosf(CUDART_PI_F * (float)th[q], &pri[q], &prr[q]);
-              else { pri[q] = 0.f; prr[q] = 1.f; }
-            }
-#pragma unroll
-            for (int hq = 0; hq < PPT / 2; ++hq) c2[hq] = make_float2(2.f * cf[2 * hq], 2.f * cf[2 * hq + 1]);
-            const float2 neg1 = make_float2(-1.f, -1.f);
-            const int n4 = Kp4 >> 2;
-            for (int gi = 0; gi < G; ++gi) {
-              // ---- each span's own K-segment recurrence (Eqs. 8-9)
-              float2 b1[PPT / 2], b2[PPT / 2];
-#pragma unroll
-              for (int hq = 0; hq < PPT / 2; ++hq) {
-                b1[hq] = make_float2(0.f, 0.f);
-                b2[hq] = make_float2(0.f, 0.f);
-              }
-              auto step = [&](float a) {
-#pragma unroll
-                for (int hq = 0; hq < PPT / 2; ++hq) {
-                  // (2cos b_{k+1} + a) - b_{k+2}: the shared a in the addend slot (operand reuse)
-                  const float2 t = __ffma2_rn(c2[hq], b1[hq], make_float2(a, a));
-                  const float2 n = __ffma2_rn(b2[hq], neg1, t);
-                  b2[hq] = b1[hq];
-                  b1[hq] = n;
-                }
-              };
-              float4 tc = rowq[0];
-#pragma unroll 2
-              for (int i4 = 0; i4 < n4 - 1; ++i4) {
-                const float4 tn = rowq[i4 + 1];
-                step(tc.x);
-                step(tc.y);
-                step(tc.z);
-                step(tc.w);
-                tc = tn;
-              }
-              step(tc.x);
-              step(tc.y);
-              step(tc.z);                                           // -> b_1, b_2
-#pragma unroll
-              for (int q = 0; q < PPT; ++q) {
-                const float bb1 = (q & 1) ? b1[q >> 1].y : b1[q >> 1].x;
-                const float bb2 = (q & 1) ? b2[q >> 1].y : b2[q >> 1].x;
-                const float accr = fmaf(cf[q], bb1, tc.w - bb2);     // a'_0 + z b_1 - b_2
-                const float acci = sf[q] * bb1;
-                const float mr = nrf[q] * accr - nif[q] * acci;      // mu_s = I_0 sum
-                const float mi = nrf[q] * acci + nif[q] * accr;
-                yr[q] += (double)fmaf(mr, prr[q], -mi * pri[q]);     // Y += gamma mu e^{i theta_s}
-                yi[q] += (double)fmaf(mr, pri[q], mi * prr[q]);
-                const float npr = fmaf(prr[q], drr[q], -pri[q] * dri[q]);
-                pri[q] = fmaf(prr[q], dri[q], pri[q] * drr[q]);
-                prr[q] = npr;
-              }
-            }
-#pragma unroll
-            for (int q = 0; q < PPT; ++q) {
-              const double t2 = fma(xs[q], (double)(Ks * G), th[q]);
-              th[q] = t2 - 2.0 * rint(0.5 * t2);
-            }
+            span_seg32(p, ch, G, cls, A2, A3, Eh, ah, gh, Ks,
+                       reinterpret_cast<const float*>(sm.T) + (li - tb) * 2 * p.tstride, uv, Ssum, yr, yi,
+                       th);
             continue;
           }
           double x[PPT], sn[PPT], cs[PPT];
@@ -737,27 +865,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
               mr = (nr * accr[q] - ni * acci[q]) * inv;
               mi = (nr * acci[q] + ni * accr[q]) * inv;
             } else {
-              // Maclaurin (Eq. 4): mu = eta - (P C f3 / alpha)(eta - eta2), eta = (e^{(i chi - a)L}-1)/(i chi - a)
-              const double aL = __ldg(p.aL + s);
-              const double xl = x[q] * Ks;        // chi L / pi
-              double sl, cl;
-              sincospi_d(xl, &sl, &cl);
-              const double e1 = exp(-aL), e2 = e1 * e1;
-              // eta / h = (e1 cis(chi L) - 1) / ((i chi - alpha) h): multiply by conj(d) / |d|^2
-              const double ar = -ah, ai = px;     // d = (i chi - alpha) h
-              const double den1 = 1.0 / fma(ai, ai, ar * ar);
-              const double n1r = fma(e1, cl, -1.0), n1i = e1 * sl;
-              const double eta_r = (n1r * ar + n1i * ai) * den1;
-              const double eta_i = (n1i * ar - n1r * ai) * den1;
-              const double br = -2.0 * ah;
-              const double den2 = 1.0 / fma(ai, ai, br * br);
-              const double n2r = fma(e2, cl, -1.0), n2i = e2 * sl;
-              const double et2_r = (n2r * br + n2i * ai) * den2;
-              const double et2_i = (n2i * br - n2r * ai) * den2;
-              const double cf = __ldg(p.mac_c + s) * f3l;
-              // (values above are eta / h; gh = gamma h restores the scale)
-              mr = (eta_r - cf * (eta_r - et2_r)) * gh;
-              mi = (eta_i - cf * (eta_i - et2_i)) * gh;
+              mu_maclaurin(p, s, x[q], px, ah, gh, Ks, f3l, &mr, &mi);
             }
             if (LG) {   // Lambda_s of the chain's first span (prefix / suffix sums)
               const double lam = exp(0.5 * (fma(-__ldg(p.lgB + s), 2.0 * f3l + f, __ldg(p.lgA + s)) +
@@ -788,59 +896,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
         for (int q = 0; q < PPT; ++q)
           sm.ybuf[PPT * tid + q] = valid[q] ? make_double2(yr[q], yi[q]) : make_double2(0.0, 0.0);
         __syncthreads();
-        // lines (G, H): one thread per line in the chunk, points in order
-        if (flags & (NEED_G | NEED_H)) {
-          for (int i = i_first + tid; i <= i_last; i += BLOCK) {
-            const int s0 = max(sm.sl_start[i], p0), s1 = min(sm.sl_start[i] + sm.sl_cnt[i], p_end);
-            double2 acc = sm.lineacc[i];
-            for (int t = s0; t < s1; ++t) {
-              const double2 y = sm.ybuf[t - p0];
-              acc.x += y.x;
-              acc.y += y.y;
-            }
-            sm.lineacc[i] = acc;
-          }
-        }
-        // rows (E): r[m2] += sum over the chunk's lines of wE Y(m1, m2), line order
-        if (flags & NEED_E) {
-          for (int m2 = tid; m2 < N; m2 += BLOCK) {
-            double2 acc = sm.rowacc[m2];
-            for (int i = i_first; i <= i_last; ++i) {
-              const double w = sm.wE[i];
-              if (w == 0.0) continue;
-              const int num = sm.sl_j[i] - b * m2;
-              if (num < 0 || num % a) continue;
-              const int m1 = num / a;
-              if (m1 >= N) continue;
-              const int idx = sm.sl_start[i] + (m1 - sm.sl_first[i]) / b;
-              if (m1 < sm.sl_first[i] || idx < p0 || idx >= p_end) continue;
-              const double2 y = sm.ybuf[idx - p0];
-              acc.x = fma(w, y.x, acc.x);
-              acc.y = fma(w, y.y, acc.y);
-            }
-            sm.rowacc[m2] = acc;
-          }
-        }
-        // columns (F): c[m1] += sum over the chunk's lines of wF Y(m1, m2)
-        if (flags & NEED_F) {
-          for (int m1 = tid; m1 < N; m1 += BLOCK) {
-            double2 acc = sm.colacc[m1];
-            for (int i = i_first; i <= i_last; ++i) {
-              const double w = sm.wF[i];
-              if (w == 0.0) continue;
-              const int num = sm.sl_j[i] - a * m1;
-              if (num < 0 || num % b) continue;
-              const int m2 = num / b;
-              if (m2 >= N || m1 < sm.sl_first[i]) continue;
-              const int idx = sm.sl_start[i] + (m1 - sm.sl_first[i]) / b;
-              if (idx < p0 || idx >= p_end) continue;
-              const double2 y = sm.ybuf[idx - p0];
-              acc.x = fma(w, y.x, acc.x);
-              acc.y = fma(w, y.y, acc.y);
-            }
-            sm.colacc[m1] = acc;
-          }
-        }
+        coherent_chunk(sm, flags, N, a, b, i_first, i_last, p0, p_end);
         __syncthreads();
       }
       p0 = p_end;
