@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <string>
 #include <tuple>
@@ -35,11 +36,19 @@ template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  bool owned = true;   // false: p points into an Arena (one allocation for many buffers)
   ~DevBuf() { reset(); }
   void reset() {
-    if (p) cudaFree(p);
+    if (p && owned) cudaFree(p);
     p = nullptr;
     n = 0;
+    owned = true;
+  }
+  void borrow(T* q, size_t cnt) {
+    reset();
+    p = q;
+    n = cnt;
+    owned = false;
   }
   bool alloc(size_t count) {
     reset();
@@ -55,6 +64,60 @@ struct DevBuf {
     if (!alloc(v.size())) return false;
     if (v.empty()) return true;
     return cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice) == cudaSuccess;
+  }
+};
+
+// One device allocation holding many small buffers (fewer cudaMalloc / cudaFree calls on the
+// create / plan path): buffers with host data are staged into one host block and copied with ONE
+// cudaMemcpy; device-only buffers follow them uninitialised.
+struct Arena {
+  char* base = nullptr;
+  ~Arena() { reset(); }
+  void reset() {
+    if (base) cudaFree(base);
+    base = nullptr;
+  }
+};
+
+class Packer {
+  struct E {
+    std::function<void(char*)> bind;
+    const void* src;
+    size_t bytes, off;
+  };
+  std::vector<E> init_, dev_;
+  static size_t up(size_t b) { return (std::max<size_t>(b, 1) + 255) & ~(size_t)255; }
+
+ public:
+  template <class T>
+  void add(DevBuf<T>* d, const std::vector<T>& v) {
+    const size_t cnt = v.size();
+    init_.push_back({[d, cnt](char* q) { d->borrow(reinterpret_cast<T*>(q), cnt); }, v.data(),
+                     cnt * sizeof(T), 0});
+  }
+  template <class T>
+  void reserve(DevBuf<T>* d, size_t cnt) {   // device-only, uninitialised
+    dev_.push_back({[d, cnt](char* q) { d->borrow(reinterpret_cast<T*>(q), cnt); }, nullptr,
+                    cnt * sizeof(T), 0});
+  }
+  bool commit(Arena* a) {
+    size_t off = 0;
+    for (auto& e : init_) { e.off = off; off += up(e.bytes); }
+    const size_t init_bytes = off;
+    for (auto& e : dev_) { e.off = off; off += up(e.bytes); }
+    a->reset();
+    if (cudaMalloc(&a->base, std::max<size_t>(off, 256)) != cudaSuccess) {
+      a->base = nullptr;
+      return false;
+    }
+    std::vector<char> stage(init_bytes);
+    for (auto& e : init_) {
+      if (e.bytes) std::memcpy(stage.data() + e.off, e.src, e.bytes);
+      e.bind(a->base + e.off);
+    }
+    for (auto& e : dev_) e.bind(a->base + e.off);
+    return init_bytes == 0 ||
+           cudaMemcpy(a->base, stage.data(), init_bytes, cudaMemcpyHostToDevice) == cudaSuccess;
   }
 };
 
@@ -102,6 +165,7 @@ struct isrs_egn {
   long long sh_lo = 0, sh_hi = 0;
   DevBuf<int> d_sh_d, d_sh_c;
   DevBuf<double> d_partials, d_npts;
+  Arena arena_create, arena_plan;   // declared after the DevBufs: destroyed first
   cudaStream_t last_stream = nullptr;
   bool have_result = false;
   int last_launches = 0;
@@ -387,19 +451,20 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
     delete h;
     return fail(ISRS_EGN_ERANGE, "grid_n / K_s exceed the shared-memory budget");
   }
-  bool ok = h->d_lo.upload(h->lo) && h->d_hi.upload(h->hi) && h->d_f.upload(h->f) &&
-            h->d_G.upload(h->G) && h->d_R.upload(h->R) && h->d_P.upload(h->P) &&
-            h->d_phi.upload(h->phi) && h->d_psi.upload(h->psi) && h->d_delta.upload(h->delta) &&
-            h->d_rate.upload(h->rate) && h->d_A2.upload(A2) && h->d_A3.upload(A3) &&
-            h->d_Eh.upload(Eh) && h->d_ah.upload(ah) && h->d_gh.upload(gh) &&
-            h->d_macc.upload(macc) && h->d_aL.upload(aL) && h->d_K.upload(K) && h->d_cls.upload(cls) &&
-            h->d_Kc.upload(cK) && h->d_chain_s0.upload(ch_s0) && h->d_chain_g.upload(ch_g) &&
-            h->d_lnc_L.upload(lncL) && h->d_zeta_L.upload(zL) && h->d_lgA.upload(lgA) &&
-            h->d_lgB.upload(lgB) && h->d_lgC.upload(lgC) && h->d_lgD.upload(lgD) &&
-            h->d_Ls.upload(vL) && h->d_alpha.upload(vA) && h->d_gamma.upload(vG) && h->d_pcr.upload(vP);
   DevBuf<double> dL, dA, dC;
-  ok = ok && dL.upload(cL) && dA.upload(cA) && dC.upload(cC) &&
-       h->d_lnA.alloc((size_t)h->n_cls * h->kstride) && h->d_zeta.alloc((size_t)h->n_cls * h->kstride);
+  Packer pk;
+  pk.add(&h->d_lo, h->lo); pk.add(&h->d_hi, h->hi); pk.add(&h->d_f, h->f); pk.add(&h->d_G, h->G);
+  pk.add(&h->d_R, h->R); pk.add(&h->d_P, h->P); pk.add(&h->d_phi, h->phi); pk.add(&h->d_psi, h->psi);
+  pk.add(&h->d_delta, h->delta); pk.add(&h->d_rate, h->rate); pk.add(&h->d_A2, A2);
+  pk.add(&h->d_A3, A3); pk.add(&h->d_Eh, Eh); pk.add(&h->d_ah, ah); pk.add(&h->d_gh, gh);
+  pk.add(&h->d_macc, macc); pk.add(&h->d_aL, aL); pk.add(&h->d_K, K); pk.add(&h->d_cls, cls);
+  pk.add(&h->d_Kc, cK); pk.add(&h->d_chain_s0, ch_s0); pk.add(&h->d_chain_g, ch_g);
+  pk.add(&h->d_lnc_L, lncL); pk.add(&h->d_zeta_L, zL); pk.add(&h->d_lgA, lgA); pk.add(&h->d_lgB, lgB);
+  pk.add(&h->d_lgC, lgC); pk.add(&h->d_lgD, lgD); pk.add(&h->d_Ls, vL); pk.add(&h->d_alpha, vA);
+  pk.add(&h->d_gamma, vG); pk.add(&h->d_pcr, vP); pk.add(&dL, cL); pk.add(&dA, cA); pk.add(&dC, cC);
+  pk.reserve(&h->d_lnA, (size_t)h->n_cls * h->kstride);
+  pk.reserve(&h->d_zeta, (size_t)h->n_cls * h->kstride);
+  const bool ok = pk.commit(&h->arena_create);
   if (!ok) {
     delete h;
     return fail(ISRS_EGN_ENOMEM, "device allocation/upload failed");
@@ -565,12 +630,12 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
     // (re)build and upload the work list for this COI set (cached across identical calls)
     cudaStreamSynchronize(h->last_stream);
     build_worklist(h, c, &h->wl);
-    bool ok = h->d_desc.upload(h->wl.desc) && h->d_coi_off.upload(h->wl.coi_off) &&
-              h->d_coi.upload(h->wl.coi) && h->d_list_d.upload(h->wl.list_d) &&
-              h->d_list_c.upload(h->wl.list_c) && h->d_fv.upload(h->wl.fv) &&
-              h->d_partials.alloc(h->wl.desc.size() * 6) &&
-              h->d_npts.alloc(c.size());
-    if (!ok) return fail(ISRS_EGN_ENOMEM, "work-list allocation failed");
+    Packer pk;
+    pk.add(&h->d_desc, h->wl.desc); pk.add(&h->d_coi_off, h->wl.coi_off); pk.add(&h->d_coi, h->wl.coi);
+    pk.add(&h->d_list_d, h->wl.list_d); pk.add(&h->d_list_c, h->wl.list_c); pk.add(&h->d_fv, h->wl.fv);
+    pk.reserve(&h->d_partials, h->wl.desc.size() * 6);
+    pk.reserve(&h->d_npts, c.size());
+    if (!pk.commit(&h->arena_plan)) return fail(ISRS_EGN_ENOMEM, "work-list allocation failed");
     h->sh_rank = h->sh_world = -1;
   }
   const int* dl_d = h->d_list_d.p;
