@@ -329,7 +329,7 @@ def run_ours(args, link, ws, rank, local):
         t_e2e = []
         if ws == 1:
             isrs.eta_host(link, device=local, precision=args.precision)     # warm-up (one-time costs)
-        for k in range(max(1, min(5, args.steps))):
+        for k in range(max(1, min(7, args.steps))):
             if ws > 1:
                 torch.distributed.barrier()
             t0 = time.perf_counter()
@@ -346,7 +346,7 @@ def run_ours(args, link, ws, rank, local):
                 torch.distributed.all_reduce(dt, op=torch.distributed.ReduceOp.MAX)
             t_e2e.append(float(dt.item()))
         e2e = {"value": pspans / float(np.median(t_e2e)), "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": 8 * n,
+               "d2h_bytes_per_step": 8 * n, "samples_ms": [round(1e3 * x, 2) for x in t_e2e],
                "note": ("isrs_egn_eta_host(): validate + region plan + H2D + precompute + nli + D2H + free"
                         if ws == 1 else "per rank: create (H2D, precompute) + nli_shard + NCCL all-gather "
                         "+ combine + D2H + destroy; max over ranks")}

@@ -28,6 +28,9 @@ constexpr int LINE_CAP = 512;       // f3-lines compacted per segment (2N-1 <= 5
 constexpr int TW_MAX = ISRS_TW;     // envelope-table rows (f3-lines) resident in smem
 constexpr int T_BYTES = ISRS_TBYTES;  // smem budget of the envelope table
 constexpr int LPT = LINE_CAP / BLOCK;  // lattice lines scanned per thread
+#ifndef ISRS_WALK
+#define ISRS_WALK 4
+#endif
 #ifndef ISRS_CHAIN_MAX
 #define ISRS_CHAIN_MAX 800
 #endif

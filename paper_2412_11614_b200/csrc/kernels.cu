@@ -369,26 +369,52 @@ __device__ __forceinline__ void build_table(const KParams& p, const Smem& sm, in
   float* T32 = reinterpret_cast<float*>(sm.T);
   const double* lnA = p.lnA + (size_t)cls * p.kstride;
   const double* zt = p.zeta + (size_t)cls * p.kstride;
-  // one thread per coefficient k walks the rows: a'_k(f3 + g) = a'_k(f3) e^{-zeta_k g}
-  // (one DMUL per entry; rows whose line index jumps restart from exp; <= tw steps,
-  // relative error <= tw eps)
+  // one thread per coefficient k walks the rows: a'_k(f3 + g) = a'_k(f3) e^{-zeta_k g}.
+  // A run of WALK consecutive lines takes every entry from the run's predecessor with one DMUL
+  // by step^m (m = 1..WALK), so the dependent chain is one DMUL per WALK rows; rows whose line
+  // index jumps restart from exp (relative error <= 2 tw eps).
+  constexpr int WALK = ISRS_WALK;
   for (int ii = tid; ii < Kp; ii += BLOCK) {
     const int k = Kp - 1 - ii;
     const bool live = k < Kc;
     const double la = live ? __ldg(lnA + k) : 0.0, ze = live ? __ldg(zt + k) : 0.0;
-    const double step = exp(-ze * g);
+    double sp[WALK];
+    sp[0] = exp(-ze * g);
+#pragma unroll
+    for (int m = 1; m < WALK; ++m) sp[m] = sp[m - 1] * sp[0];
     double v = 0.0;
     int jprev = -2;
-    for (int row = 0; row < tn; ++row) {
-      const int j = sm.sl_j[tb + row];
-      if (live) v = (j == jprev + 1) ? v * step : exp(la - ze * __dadd_rn(C, g * (double)j));
-      jprev = j;
+    int row = 0;
+    auto put = [&](int r, double x) {
       if (F32) {
-        T32[row * 2 * p.tstride + ii] = (float)v;
+        T32[r * 2 * p.tstride + ii] = (float)x;
       } else {
-        sm.T[row * p.tstride + ii] = v;
-        if (ii < 2) sm.T[row * p.tstride + Kp + ii] = v;   // wrap pair for span chains (R9)
+        sm.T[r * p.tstride + ii] = x;
+        if (ii < 2) sm.T[r * p.tstride + Kp + ii] = x;   // wrap pair for span chains (R9)
       }
+    };
+    while (row < tn) {
+      if (WALK > 1 && row + WALK <= tn) {
+        int jr[WALK];
+#pragma unroll
+        for (int m = 0; m < WALK; ++m) jr[m] = sm.sl_j[tb + row + m];
+        if (jr[0] == jprev + 1 && jr[WALK - 1] == jr[0] + WALK - 1) {   // block-uniform
+          double vr[WALK];
+#pragma unroll
+          for (int m = 0; m < WALK; ++m) vr[m] = v * sp[m];
+#pragma unroll
+          for (int m = 0; m < WALK; ++m) put(row + m, vr[m]);
+          v = vr[WALK - 1];
+          jprev = jr[WALK - 1];
+          row += WALK;
+          continue;
+        }
+      }
+      const int j = sm.sl_j[tb + row];
+      if (live) v = (j == jprev + 1) ? v * sp[0] : exp(la - ze * __dadd_rn(C, g * (double)j));
+      jprev = j;
+      put(row, v);
+      ++row;
     }
   }
 }
