@@ -693,8 +693,8 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
   int launches = 0;
 #ifdef ISRS_PROF
   static unsigned long long* d_prof = nullptr;
-  if (!d_prof) cudaMalloc(&d_prof, 8 * sizeof(unsigned long long));
-  cudaMemsetAsync(d_prof, 0, 8 * sizeof(unsigned long long), st);
+  if (!d_prof) cudaMalloc(&d_prof, 16 * sizeof(unsigned long long));
+  cudaMemsetAsync(d_prof, 0, 16 * sizeof(unsigned long long), st);
   kp.prof = d_prof;
 #endif
   if (!h->side) {
@@ -729,7 +729,7 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
   cudaEventRecord(h->ev[3], st);
 #ifdef ISRS_PROF
   {
-    unsigned long long hp[8];
+    unsigned long long hp[16];
     cudaMemcpyAsync(hp, d_prof, sizeof(hp), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     double tot = 0;
@@ -739,6 +739,9 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
     fprintf(stderr, "ISRS_PROF warp-cycles:");
     for (int i = 0; i < 7; ++i) fprintf(stderr, " %s %.2f%%", nm[i], 100.0 * hp[i] / tot);
     fprintf(stderr, " (total %.3e)\n", tot);
+    fprintf(stderr, "ISRS_PROF table builds %llu, mean rows %.2f; chunks %llu, mean slots %.1f, mean lines %.2f\n",
+            hp[8], hp[8] ? (double)hp[9] / hp[8] : 0.0, hp[10], hp[10] ? (double)hp[11] / hp[10] : 0.0,
+            hp[10] ? (double)hp[12] / hp[10] : 0.0);
   }
 #endif
   launches += 1;

@@ -44,10 +44,12 @@
 // phase timers (debug builds only, -DISRS_PROF): per-warp clock64 deltas summed into p.prof
 #define PROF_DECL unsigned long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long prof_t = clock64();
 #define PROF_MARK(i) { const long long t_ = clock64(); prof_acc[i] += (unsigned long long)(t_ - prof_t); prof_t = t_; }
+#define PROF_COUNT(i, v) { if (threadIdx.x == 0 && p.prof) atomicAdd(p.prof + (i), (unsigned long long)(v)); }
 #define PROF_FLUSH if ((threadIdx.x & 31) == 0 && p.prof) { for (int i_ = 0; i_ < 8; ++i_) atomicAdd(p.prof + i_, prof_acc[i_]); }
 #else
 #define PROF_DECL
 #define PROF_MARK(i)
+#define PROF_COUNT(i, v)
 #define PROF_FLUSH
 #endif
 #define ISRS_STR(x) #x
@@ -374,6 +376,18 @@ __device__ __forceinline__ void build_table(const KParams& p, const Smem& sm, in
   // by step^m (m = 1..WALK), so the dependent chain is one DMUL per WALK rows; rows whose line
   // index jumps restart from exp (relative error <= 2 tw eps).
   constexpr int WALK = ISRS_WALK;
+  static_assert(TW_MAX <= 64, "the restart mask holds one bit per table row");
+  // restart mask (per warp, by ballot): bit r set when row r does not continue its predecessor's
+  // line (j_r != j_{r-1} + 1; row 0 always), so the walk's control flow reads no shared memory
+  unsigned long long rmask;
+  {
+    const int lane = tid & 31;
+    const int r0 = lane, r1 = lane + 32;
+    const bool b0 = (r0 >= tn) || r0 == 0 || sm.sl_j[tb + r0] != sm.sl_j[tb + r0 - 1] + 1;
+    const bool b1 = (r1 >= tn) || sm.sl_j[tb + r1] != sm.sl_j[tb + r1 - 1] + 1;
+    rmask = (unsigned long long)__ballot_sync(0xffffffffu, b0) |
+            ((unsigned long long)__ballot_sync(0xffffffffu, b1) << 32);
+  }
   for (int ii = tid; ii < Kp; ii += BLOCK) {
     const int k = Kp - 1 - ii;
     const bool live = k < Kc;
@@ -383,7 +397,6 @@ __device__ __forceinline__ void build_table(const KParams& p, const Smem& sm, in
 #pragma unroll
     for (int m = 1; m < WALK; ++m) sp[m] = sp[m - 1] * sp[0];
     double v = 0.0;
-    int jprev = -2;
     int row = 0;
     auto put = [&](int r, double x) {
       if (F32) {
@@ -394,25 +407,23 @@ __device__ __forceinline__ void build_table(const KParams& p, const Smem& sm, in
       }
     };
     while (row < tn) {
-      if (WALK > 1 && row + WALK <= tn) {
-        int jr[WALK];
+      const unsigned long long rest = rmask >> row;
+      if (WALK > 1 && row + WALK <= tn && (rest & ((1ull << WALK) - 1ull)) == 0ull) {   // block-uniform
+        double vr[WALK];
 #pragma unroll
-        for (int m = 0; m < WALK; ++m) jr[m] = sm.sl_j[tb + row + m];
-        if (jr[0] == jprev + 1 && jr[WALK - 1] == jr[0] + WALK - 1) {   // block-uniform
-          double vr[WALK];
+        for (int m = 0; m < WALK; ++m) vr[m] = v * sp[m];
 #pragma unroll
-          for (int m = 0; m < WALK; ++m) vr[m] = v * sp[m];
-#pragma unroll
-          for (int m = 0; m < WALK; ++m) put(row + m, vr[m]);
-          v = vr[WALK - 1];
-          jprev = jr[WALK - 1];
-          row += WALK;
-          continue;
-        }
+        for (int m = 0; m < WALK; ++m) put(row + m, vr[m]);
+        v = vr[WALK - 1];
+        row += WALK;
+        continue;
       }
-      const int j = sm.sl_j[tb + row];
-      if (live) v = (j == jprev + 1) ? v * sp[0] : exp(la - ze * __dadd_rn(C, g * (double)j));
-      jprev = j;
+      if (rest & 1ull) {
+        const int j = sm.sl_j[tb + row];
+        if (live) v = exp(la - ze * __dadd_rn(C, g * (double)j));
+      } else {
+        v *= sp[0];
+      }
       put(row, v);
       ++row;
     }
@@ -715,6 +726,9 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
       const int lim = min(i_first + p.tw, S);
       const int p_end = min(p0 + CP, sm.sl_start[lim]);
       const int i_last = line_of(sm.sl_start, lim - 1, p_end - 1, i_first);
+      PROF_COUNT(10, 1)
+      PROF_COUNT(11, p_end - p0)
+      PROF_COUNT(12, i_last - i_first + 1)
 
       // ---- per-thread points: PPT consecutive slots of one line (lines are padded to whole
       // groups), so one envelope-table row serves all PPT recurrences of the thread
@@ -773,6 +787,8 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
             tn = (p.n_cls == 1) ? min(p.tw, S - i_first) : (i_last - i_first + 1);
             tcls = cls;
             build_table<MODE == MODE_SEG32>(p, sm, cls, tb, tn, C, g);
+            PROF_COUNT(8, 1)
+            PROF_COUNT(9, tn)
             __syncthreads();
           }
           PROF_MARK(3)   // table (re)build incl. barriers
