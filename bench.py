@@ -223,7 +223,8 @@ def config_desc(link, args):
             "n_coi": link.n_ch, "seed": link.seed,
             "l2": "flushed between timed steps (256 MiB write, outside the step events)",
             "parallelism": (f"region shards x{args.gpus} (cost-balanced contiguous shards of one link, "
-                            "NCCL all-gather of per-COI sums, fixed-order combine; strong scaling)"
+                            f"{(args.backend or 'nccl').upper()} all-gather of per-COI sums, fixed-order combine; "
+                            "strong scaling)"
                             if args.gpus > 1 else "1 GPU")}
 
 
@@ -348,7 +349,7 @@ def run_ours(args, link, ws, rank, local):
         e2e = {"value": pspans / float(np.median(t_e2e)), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 8 * n, "samples_ms": [round(1e3 * x, 2) for x in t_e2e],
                "note": ("isrs_egn_eta_host(): validate + region plan + H2D + precompute + nli + D2H + free"
-                        if ws == 1 else "per rank: create (H2D, precompute) + nli_shard + NCCL all-gather "
+                        if ws == 1 else f"per rank: create (H2D, precompute) + nli_shard + {(args.backend or 'nccl').upper()} all-gather "
                         "+ combine + D2H + destroy; max over ranks")}
 
     # NEXT-4a, reported separately (never the headline): span-class dedup evaluates each run of
