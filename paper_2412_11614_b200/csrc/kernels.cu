@@ -752,11 +752,16 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
       bool valid[PPT];
       double uv[PPT], Ssum[PPT];
       const double f3l = __dadd_rn(C, g * (double)lj);
+      // the line's first point (m1f, m2f): one exact division per thread; along the line
+      // m1 steps by b and m2 by -a
+      const int m1f = sm.sl_first[li];
+      const int m2f = (b == 1) ? lj - a * m1f : (lj - a * m1f) / b;
 #pragma unroll
       for (int q = 0; q < PPT; ++q) {
         valid[q] = gvalid && (kq0 + q < lcnt);
-        const int m1 = sm.sl_first[li] + b * (valid[q] ? kq0 + q : 0);
-        const int m2 = (lj - a * m1) / b;
+        const int step_q = valid[q] ? kq0 + q : 0;
+        const int m1 = m1f + b * step_q;
+        const int m2 = m2f - a * step_q;
         const double f1 = __dadd_rn(lo1, __dmul_rn((double)m1 + 0.5, d1));   // C6 bin centres
         const double f2 = __dadd_rn(lo2, __dmul_rn((double)m2 + 0.5, d2));
         const double u = __dadd_rn(f1, -f), w = __dadd_rn(f2, -f);
