@@ -97,6 +97,64 @@ def test_eta_parity_edge_cases(isrs, name):
     assert np.all(np.abs(t_g - t_o) <= TOL_ETA * scale), name
 
 
+def random_tiny_kwargs(seed):
+    """Seeded random small link: 1-5 channels with rates drawn from {16..96} GBd (lattice ratios up
+    to 6:1), guard-packed (incl. touching bands) or on a uniform plan, 1-5 spans (identical or
+    drawn), N in {8, 10, 16, 20}, dz in {1, 2.5, 5} km, C_r in {0, 0.028, 0.28} /W/km/THz, tilted
+    powers, mixed formats."""
+    rng = np.random.default_rng(1000 + seed)
+    n_ch = int(rng.integers(1, 6))
+    rates = tuple(int(x) for x in rng.choice([16, 32, 48, 64, 96], size=int(rng.integers(1, 4))))
+    kw = dict(n_ch=n_ch, rates_gbd=rates, n_span=int(rng.integers(1, 6)),
+              grid_n=int(rng.choice([8, 10, 16, 20])), random_spans=bool(rng.integers(0, 2)),
+              cr_w_km_thz=float(rng.choice([0.0, 0.028, 0.28])), power_dbm=float(rng.uniform(-2, 4)),
+              tilt_db=float(rng.uniform(-3, 3)), seed=seed,
+              fmts=tuple(rng.choice(["gauss", "qpsk", "16qam", "64qam"], size=3)))
+    if rng.integers(0, 2):
+        kw["guard_ghz"] = float(rng.choice([0.0, 12.5, 25.0, 50.0]))
+    else:
+        kw["spacing_ghz"] = float(max(rates) + rng.choice([0, 4, 36]))
+    return kw, float(rng.choice([1000.0, 2500.0, 5000.0]))
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_eta_parity_random_links(isrs, seed):
+    kw, dz = random_tiny_kwargs(seed)
+    link = tiny_link(**kw).with_(delta_z_m=dz)
+    e_o, t_o = egn.eta(link)
+    e_g, t_g = gpu_eta(isrs, link)
+    rel = np.abs(e_g - e_o) / e_o
+    assert np.all(rel <= TOL_ETA), (seed, kw, rel)
+    scale = np.abs(t_o).sum(axis=1, keepdims=True)
+    assert np.all(np.abs(t_g - t_o) <= TOL_ETA * scale), (seed, kw)
+
+
+RANDOM_MODES = {
+    # mode: (oracle kwargs, Engine kwargs builder, tolerance kind)
+    "dedup": ({}, lambda m: {"flags": m.FLAG_DEDUP}, "rel"),
+    "literal_gain": ({"gain": "literal"}, lambda m: {"flags": m.FLAG_LITERAL_GAIN}, "rel"),
+    "maclaurin": ({"mu_mode": "maclaurin"}, lambda m: {"mu_mode": m.MU_MACLAURIN}, "rel"),
+    "no_chain": ({}, lambda m: {"flags": m.FLAG_NO_CHAIN}, "rel"),
+    "fp32": ({}, lambda m: {"precision": 32}, "db"),
+    "3d_f2": ({"f_samples": 2}, lambda m: {"f_samples": 2}, "rel"),
+}
+
+
+@pytest.mark.parametrize("mode", sorted(RANDOM_MODES))
+@pytest.mark.parametrize("seed", range(8))
+def test_modes_parity_random_links(isrs, seed, mode):
+    """Every option of the ABI on the seeded random links: the same oracle bar as its fixed tests."""
+    kw, dz = random_tiny_kwargs(seed)
+    link = tiny_link(**kw).with_(delta_z_m=dz)
+    okw, ekw, kind = RANDOM_MODES[mode]
+    e_o, _ = egn.eta(link, **okw)
+    e_g, _ = gpu_eta(isrs, link, **ekw(isrs))
+    if kind == "rel":
+        assert np.all(np.abs(e_g - e_o) / e_o <= TOL_ETA), (seed, mode, np.abs(e_g - e_o) / e_o)
+    else:
+        assert np.all(np.abs(10 * np.log10(e_g / e_o)) <= 1e-3), (seed, mode, 10 * np.log10(e_g / e_o))
+
+
 def test_degenerate_zero_gamma_and_empty_coi(isrs):
     """gamma = 0 in every span: Y = 0, eta = 0 exactly; an empty COI list is rejected."""
     link = tiny_link(n_ch=3, rates_gbd=(64,), n_span=2, grid_n=8, fmts=("16qam",))
