@@ -31,6 +31,21 @@ constexpr int LPT = LINE_CAP / BLOCK;  // lattice lines scanned per thread
 #ifndef ISRS_WALK
 #define ISRS_WALK 4
 #endif
+// -DISRS_CHECK: device-side bounds checks on every shared-memory index family (debug builds; the
+// pool has no compute-sanitizer), a violation prints the site and traps
+#ifdef ISRS_CHECK
+#define ISRS_BOUND(i, n)                                                                        \
+  do {                                                                                          \
+    if (!((unsigned)(i) < (unsigned)(n))) {                                                     \
+      printf("ISRS_CHECK %s:%d %s = %d not in [0, %d)\n", __FILE__, __LINE__, #i, (int)(i), (int)(n)); \
+      __trap();                                                                                 \
+    }                                                                                           \
+  } while (0)
+#else
+#define ISRS_BOUND(i, n) \
+  do {                   \
+  } while (0)
+#endif
 #ifndef ISRS_CHAIN_MAX
 #define ISRS_CHAIN_MAX 800
 #endif

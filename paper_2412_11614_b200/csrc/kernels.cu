@@ -343,6 +343,7 @@ __device__ __forceinline__ int4 scan_lines(const KParams& p, const Smem& sm, int
 #pragma unroll
   for (int q = 0; q < LPT; ++q) {
     if (cnt[q] > 0) {
+      ISRS_BOUND(pos.x, LINE_CAP);
       sm.sl_j[pos.x] = seg0 + LPT * tid + q;
       sm.sl_first[pos.x] = first[q];
       sm.sl_start[pos.x] = pos.y;
@@ -369,6 +370,9 @@ __device__ __forceinline__ void build_table(const KParams& p, const Smem& sm, in
   // multiple of 4 (float4 loads), row stride 2 tstride floats
   const int Kp = F32 ? ((Kc + 3) & ~3) : ((Kc + 1) & ~1);
   float* T32 = reinterpret_cast<float*>(sm.T);
+  ISRS_BOUND(tn - 1, p.tw);
+  ISRS_BOUND(tb + tn - 1, LINE_CAP);
+  if (F32) ISRS_BOUND(Kp - 1, 2 * p.tstride); else ISRS_BOUND(Kp + 1, p.tstride);
   const double* lnA = p.lnA + (size_t)cls * p.kstride;
   const double* zt = p.zeta + (size_t)cls * p.kstride;
   // one thread per coefficient k walks the rows: a'_k(f3 + g) = a'_k(f3) e^{-zeta_k g}.
@@ -442,6 +446,7 @@ __device__ __forceinline__ void coherent_chunk(const Smem& sm, int flags, int N,
       const int s0 = max(sm.sl_start[i], p0), s1 = min(sm.sl_start[i] + sm.sl_cnt[i], p_end);
       double2 acc = sm.lineacc[i];
       for (int t = s0; t < s1; ++t) {
+        ISRS_BOUND(t - p0, CP);
         const double2 y = sm.ybuf[t - p0];
         acc.x += y.x;
         acc.y += y.y;
@@ -462,6 +467,7 @@ __device__ __forceinline__ void coherent_chunk(const Smem& sm, int flags, int N,
         if (m1 >= N) continue;
         const int idx = sm.sl_start[i] + (m1 - sm.sl_first[i]) / b;
         if (m1 < sm.sl_first[i] || idx < p0 || idx >= p_end) continue;
+        ISRS_BOUND(idx - p0, CP);
         const double2 y = sm.ybuf[idx - p0];
         acc.x = fma(w, y.x, acc.x);
         acc.y = fma(w, y.y, acc.y);
@@ -482,6 +488,7 @@ __device__ __forceinline__ void coherent_chunk(const Smem& sm, int flags, int N,
         if (m2 >= N || m1 < sm.sl_first[i]) continue;
         const int idx = sm.sl_start[i] + (m1 - sm.sl_first[i]) / b;
         if (idx < p0 || idx >= p_end) continue;
+        ISRS_BOUND(idx - p0, CP);
         const double2 y = sm.ybuf[idx - p0];
         acc.x = fma(w, y.x, acc.x);
         acc.y = fma(w, y.y, acc.y);
@@ -726,6 +733,8 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
       const int lim = min(i_first + p.tw, S);
       const int p_end = min(p0 + CP, sm.sl_start[lim]);
       const int i_last = line_of(sm.sl_start, lim - 1, p_end - 1, i_first);
+      ISRS_BOUND(i_last, S);
+      ISRS_BOUND(i_first, i_last + 1);
       PROF_COUNT(10, 1)
       PROF_COUNT(11, p_end - p0)
       PROF_COUNT(12, i_last - i_first + 1)
@@ -806,6 +815,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
             continue;
           }
           if (MODE == MODE_SEG32) {
+            ISRS_BOUND(li - tb, tn);
             span_seg32(p, ch, G, cls, A2, A3, Eh, ah, gh, Ks,
                        reinterpret_cast<const float*>(sm.T) + (li - tb) * 2 * p.tstride, uv, Ssum, yr, yi,
                        th);
@@ -830,6 +840,8 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
             }
             const double2* rowp = (const double2*)(sm.T + (li - tb) * p.tstride);
             const int npair = Kp >> 1;
+            ISRS_BOUND(li - tb, tn);
+            ISRS_BOUND(npair, p.tstride / 2);
             // software-pipelined: the 16-byte loads of pair i2+1 are in flight while the PPT
             // independent recurrences of pair i2 run interleaved (LDS latency ~29 cycles)
             // span chain (R9): the coefficients of G identical spans repeat with period K, so
