@@ -18,7 +18,10 @@ constexpr int BLOCK = ISRS_BLOCK;   // threads per CTA (4 warps; 3 CTAs per SM, 
 constexpr int PPT = ISRS_PPT;       // grid points per thread in flight (independent Goertzel chains)
 constexpr int MIN_BLOCKS = ISRS_MINB;  // __launch_bounds__ min CTAs per SM
 constexpr int CP = BLOCK * PPT;     // points per chunk
-constexpr int LINE_CAP = 512;       // f3-lines compacted per segment (2N-1 <= 511 at N = 256)
+#ifndef ISRS_LINE_CAP
+#define ISRS_LINE_CAP 512
+#endif
+constexpr int LINE_CAP = ISRS_LINE_CAP;  // f3-lines compacted per segment (2N-1 <= 511 at N = 256)
 #ifndef ISRS_TW
 #define ISRS_TW 64
 #endif
@@ -55,6 +58,8 @@ constexpr int CHAIN_MAX = ISRS_CHAIN_MAX;
 // largest a + b of a channel-pair rate ratio a:b (lowest terms) the lattice line scan accepts
 constexpr long long RATIO_MAX = 64;
 static_assert(LINE_CAP % BLOCK == 0, "LINE_CAP must be a multiple of BLOCK");
+static_assert(BLOCK % 32 == 0 && (BLOCK & (BLOCK - 1)) == 0 && BLOCK <= 1024,
+              "BLOCK must be a power-of-two number of whole warps (fixed-tree block_sum)");
 
 // region flags (reading C8: a term whose gate or weight is zero is not evaluated); bits >= 8
 // hold the index of the region's NLI frequency f in KParams::fv (COI centre, or one of the
