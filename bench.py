@@ -117,6 +117,7 @@ class ClockSampler:
             self.proc.kill()
         self.t.join(timeout=2)
         sm = []
+        pw = []
         reasons = set()
         smax = None
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -126,13 +127,17 @@ class ClockSampler:
                 smax = float(r[1])
             except (ValueError, IndexError):
                 continue
+            try:
+                pw.append(float(r[2]))
+            except (ValueError, IndexError):
+                pass
             for nm, v in zip(names, r[4:8]):
                 if v.strip().lower() == "active":
                     reasons.add(nm)
         if not sm:
             return None
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w": float(np.median(pw)) if pw else None}
 
 
 def dist_setup(args):
