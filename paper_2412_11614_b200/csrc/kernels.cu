@@ -582,8 +582,8 @@ __device__ __forceinline__ void span_seg32(const KParams& p, int ch, int G, int 
                                            double (&yr)[PPT], double (&yi)[PPT], double (&th)[PPT]) {
   // ---- row a8: mixed fp32 variant (no span chains).  chi h / pi and its reduction
   // mod 2 stay fp64 (exact); z = cis(pi r) by sincospif; the recurrence runs on pairs
-  // of points with packed FFMA2; I_0, mu and the span phase factor in fp32; the phase
-  // advance and Y accumulate in fp64.
+  // of points with packed FFMA2; I_0, mu, the span phase factor and the run's Y sum in fp32;
+  // the phase advance and Y across runs in fp64.
   const float Ehf = (float)Eh, ahf = (float)ah, ghf = (float)gh;
   const int Kp4 = (__ldg(p.Kc + cls) + 3) & ~3;
   const float4* rowq = reinterpret_cast<const float4*>(rowf);
@@ -612,6 +612,10 @@ __device__ __forceinline__ void span_seg32(const KParams& p, int ch, int G, int 
   for (int hq = 0; hq < PPT / 2; ++hq) c2[hq] = make_float2(2.f * cf[2 * hq], 2.f * cf[2 * hq + 1]);
   const float2 neg1 = make_float2(-1.f, -1.f);
   const int n4 = Kp4 >> 2;
+  // the run's Y contribution in fp32 (<= CHAIN_MAX / K spans), added to the fp64 Y once per run
+  float ayr[PPT], ayi[PPT];
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) ayr[q] = ayi[q] = 0.f;
   for (int gi = 0; gi < G; ++gi) {
     // ---- each span's own K-segment recurrence (Eqs. 8-9)
     float2 b1[PPT / 2], b2[PPT / 2];
@@ -651,8 +655,8 @@ __device__ __forceinline__ void span_seg32(const KParams& p, int ch, int G, int 
       const float acci = sf[q] * bb1;
       const float mr = nrf[q] * accr - nif[q] * acci;      // mu_s = I_0 sum
       const float mi = nrf[q] * acci + nif[q] * accr;
-      yr[q] += (double)fmaf(mr, prr[q], -mi * pri[q]);     // Y += gamma mu e^{i theta_s}
-      yi[q] += (double)fmaf(mr, pri[q], mi * prr[q]);
+      ayr[q] += fmaf(mr, prr[q], -mi * pri[q]);            // Y += gamma mu e^{i theta_s}
+      ayi[q] += fmaf(mr, pri[q], mi * prr[q]);
       const float npr = fmaf(prr[q], drr[q], -pri[q] * dri[q]);
       pri[q] = fmaf(prr[q], dri[q], pri[q] * drr[q]);
       prr[q] = npr;
@@ -660,6 +664,8 @@ __device__ __forceinline__ void span_seg32(const KParams& p, int ch, int G, int 
   }
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
+    yr[q] += (double)ayr[q];
+    yi[q] += (double)ayi[q];
     const double t2 = fma(xs[q], (double)(Ks * G), th[q]);
     th[q] = t2 - 2.0 * rint(0.5 * t2);
   }

@@ -9,7 +9,7 @@ import paper_2412_11614_b200 as isrs
 from workloads import bj_config
 link = bj_config(CFG)
 coi = COI
-e = isrs.Engine(link)
+e = isrs.Engine(link, precision=PREC)
 for _ in range(2): e.nli(coi=coi)
 torch.cuda.synchronize()
 ms = []
@@ -23,13 +23,14 @@ print(json.dumps({"phase_ms": ph, "D_ms": d, "coh_ms": c, "ps_D": ps[0], "ps_all
                   "eta0": float(eta[0])}))
 '''
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
-cfg = "c2"; coi = None; reps = 3
+cfg = "c2"; coi = None; reps = 3; prec = 64
 for a in sys.argv[1:]:
     if a.startswith("--config="): cfg = a.split("=")[1]
     if a.startswith("--coi="): coi = [int(x) for x in a.split("=")[1].split(",")]
     if a.startswith("--reps="): reps = int(a.split("=")[1])
+    if a.startswith("--precision="): prec = int(a.split("=")[1])
 for lib in args:
-    code = CHILD.replace("ROOT", repr(ROOT)).replace("CFG", repr(cfg)).replace("COI", repr(coi)).replace("REPS", str(reps))
+    code = CHILD.replace("ROOT", repr(ROOT)).replace("CFG", repr(cfg)).replace("COI", repr(coi)).replace("REPS", str(reps)).replace("PREC", str(prec))
     env = dict(os.environ, ISRS_EGN_LIB=os.path.abspath(lib))
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env)
     out = r.stdout.strip().splitlines()
