@@ -14,6 +14,8 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <mutex>
+#include <set>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -32,6 +34,39 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+// Device allocations come from the device's default stream-ordered memory pool with the release
+// threshold raised, so repeated create / destroy (the one-shot isrs_egn_eta_host path) reuse pool
+// memory instead of mapping and unmapping it through the driver each time.  Allocation is on the
+// legacy default stream and completed before the buffer is handed out; frees follow a device
+// synchronisation (the buffer may be in use on any stream), as cudaFree would.
+static cudaError_t dev_alloc(void** p, size_t bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  {
+    static std::mutex mu;
+    static std::set<int> tuned;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!tuned.count(dev)) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      tuned.insert(dev);
+    }
+  }
+  e = cudaMallocAsync(p, bytes, 0);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+  return e;
+}
+
+static void dev_free(void* p) {
+  if (!p) return;
+  cudaDeviceSynchronize();
+  cudaFreeAsync(p, 0);
+}
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -39,7 +74,7 @@ struct DevBuf {
   bool owned = true;   // false: p points into an Arena (one allocation for many buffers)
   ~DevBuf() { reset(); }
   void reset() {
-    if (p && owned) cudaFree(p);
+    if (p && owned) dev_free(p);
     p = nullptr;
     n = 0;
     owned = true;
@@ -53,10 +88,12 @@ struct DevBuf {
   bool alloc(size_t count) {
     reset();
     if (count == 0) count = 1;
-    if (cudaMalloc(&p, count * sizeof(T)) != cudaSuccess) {
+    void* q = nullptr;
+    if (dev_alloc(&q, count * sizeof(T)) != cudaSuccess) {
       p = nullptr;
       return false;
     }
+    p = static_cast<T*>(q);
     n = count;
     return true;
   }
@@ -74,7 +111,7 @@ struct Arena {
   char* base = nullptr;
   ~Arena() { reset(); }
   void reset() {
-    if (base) cudaFree(base);
+    if (base) dev_free(base);
     base = nullptr;
   }
 };
@@ -106,10 +143,12 @@ class Packer {
     const size_t init_bytes = off;
     for (auto& e : dev_) { e.off = off; off += up(e.bytes); }
     a->reset();
-    if (cudaMalloc(&a->base, std::max<size_t>(off, 256)) != cudaSuccess) {
+    void* q = nullptr;
+    if (dev_alloc(&q, std::max<size_t>(off, 256)) != cudaSuccess) {
       a->base = nullptr;
       return false;
     }
+    a->base = static_cast<char*>(q);
     std::vector<char> stage(init_bytes);
     for (auto& e : init_) {
       if (e.bytes) std::memcpy(stage.data() + e.off, e.src, e.bytes);
@@ -914,10 +953,10 @@ extern "C" int isrs_egn_eta_host(const isrs_egn_problem* p, const isrs_egn_numer
   if (rc) return rc;
   const int nco = coi ? n_coi : p->n_ch;
   double* d = nullptr;
-  cudaError_t ce = cudaMalloc(&d, sizeof(double) * (size_t)nco * 6);
+  cudaError_t ce = dev_alloc(reinterpret_cast<void**>(&d), sizeof(double) * (size_t)nco * 6);
   if (ce != cudaSuccess) {
     isrs_egn_destroy(h);
-    return cuda_fail(ce, "cudaMalloc");
+    return cuda_fail(ce, "device allocation");
   }
   rc = isrs_egn_nli(h, nco, coi, d, terms_host ? d + nco : nullptr, nullptr);
   if (rc == 0) {
@@ -926,7 +965,7 @@ extern "C" int isrs_egn_eta_host(const isrs_egn_problem* p, const isrs_egn_numer
       ce = cudaMemcpy(terms_host, d + nco, sizeof(double) * nco * 5, cudaMemcpyDeviceToHost);
     if (ce != cudaSuccess) rc = cuda_fail(ce, "result copy");
   }
-  cudaFree(d);
+  dev_free(d);
   isrs_egn_destroy(h);
   return rc;
 }
