@@ -1,6 +1,6 @@
 """Pins of the oracle against what the paper and the mathematics fix (no GPU).
 
-Each test names the pin and the passage it follows.  A plausible
+Each test names the pin (this build's P14-P16) and the passage it follows.  A plausible
 mistake in the oracle (dropped term, wrong sign or index, transposed operand) must fail
 at least one of these.
 """
@@ -66,6 +66,19 @@ def test_P8_delta_rho_printed_values(row):
     assert abs(v - row["value"]) <= GOLDEN["delta_rho_tolerance_db"], (v, row["cite"])
 
 
+def test_P8_canonical_totals_of_table_I():
+    # reading C5 on the paper's Table I link: P_tot is the SUM of the launch powers
+    # (19 dBm total over 101 channels) and B_tot the edge-to-edge occupied band, which the paper
+    # rounds to "B_tot = 1 THz"; with those totals Eq. 12 gives the printed 8.2 dB up to
+    # that rounding
+    link = paper_analog("I", cr_w_km_thz=1.12)
+    c = egn.canonicalize(link)
+    assert abs(10.0 * math.log10(c.p_tot / 1e-3) - 19.0) < 1e-9
+    assert abs(c.b_tot - (100 * 10.1e9 + 10e9)) < 1.0 and abs(c.b_tot / 1e12 - 1.0) < 0.025
+    v = isrs.delta_rho_db(100e3, c.spans[0]["alpha"], c.p_tot, c.spans[0]["cr"], c.b_tot)
+    assert abs(v - 8.2) < 0.25, v
+
+
 def test_P8_power_conservation_and_tilt():
     # (1/B) int_{-B/2}^{B/2} rho(z,f) df = e^{-alpha z} (sinh normalisation of Eq. 13/25)
     a, p, cr, B = units.alpha_db_km_to_np_m(0.2), 0.316, 2.8e-17, 20e12
@@ -107,6 +120,27 @@ def test_P1_segment_with_cr0_is_gn_closed_form():
     # Maclaurin (Eq. 4) and quad (Eq. 23) reduce to the same closed form
     assert _rel(fwm.mu_maclaurin(f1, f2, f, sp, 0.1, 4e12), gn) < 1e-15
     assert _rel(fwm.mu_quad(f1[:20], f2[:20], f, sp, 0.1, 4e12), gn[:20]) < 1e-11
+
+
+def test_P16_chi_is_the_taylor_phase_mismatch():
+    # Eq. 5 abbreviates the FWM phase mismatch of the Taylor-expanded propagation
+    # constant beta(w) = beta2 w^2/2 + beta3 w^3/6 (w = 2 pi f, offsets from f_c, reading C5):
+    # chi = -(beta(w1) + beta(w2) - beta(w) - beta(w1 + w2 - w)) (sign as printed, reading C4).
+    # Built here from beta itself, not from Eq. 5's factored form.
+    f1, f2, f = _points(n=500, B=10e12, seed=11)
+    b2, b3 = SPAN["beta2"], SPAN["beta3"]
+
+    def beta(fr):
+        w = 2.0 * math.pi * fr
+        return b2 * w ** 2 / 2.0 + b3 * w ** 3 / 6.0
+    mismatch = beta(f1) + beta(f2) - beta(f) - beta(f1 + f2 - f)
+    scale = abs(b2) * (2.0 * math.pi * 10e12) ** 2
+    ch = fwm.chi(f1, f2, f, b2, b3)
+    assert np.allclose(ch, -mismatch, rtol=1e-9, atol=1e-12 * scale)
+    # the beta3 part on its own (beta2 = 0): (w1 - w)(w2 - w)(w1 + w2) beta3 / 2
+    ch3 = fwm.chi(f1, f2, f, 0.0, b3)
+    w1, w2, w = 2 * math.pi * f1, 2 * math.pi * f2, 2 * math.pi * f
+    assert np.allclose(ch3, (w1 - w) * (w2 - w) * (w1 + w2) * b3 / 2.0, rtol=1e-12, atol=0.0)
 
 
 def test_P3_peak_efficiency_is_one():
