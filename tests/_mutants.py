@@ -261,6 +261,88 @@ MUTANTS.update({
 })
 
 
+def _region_islands_with(slip):
+    """egn.region_islands (Eqs. 17-21, C6, C7, C10) with one slip in the island sums."""
+    def region_islands(c, kappa, k1, k2, mu_mode="closed", need=("D", "E", "F", "G", "H"), f=None,
+                       gain="ideal"):
+        from oracle import egn, link as link_mod
+        f = c.f[kappa] if f is None else f
+        F1, F2, f3 = egn.region_points(c, kappa, k1, k2, f)
+        if slip == "f3_plus_f":
+            f3 = F1 + F2 + f
+        gates = egn.island_gates(c, f3)
+        if not gates:
+            return []
+        support = np.zeros(f3.shape, dtype=bool)
+        for _, t in gates:
+            support |= t > 0
+        Y = np.zeros(f3.shape, dtype=np.complex128)
+        if mu_mode == "unit":
+            Y[support] = 1.0
+        else:
+            Y[support] = link_mod.link_function(F1[support], F2[support], f, c.spans, c.p_tot, c.b_tot, c.dz,
+                                                mu_mode, gain)
+        d1, d2 = c.delta[k1], c.delta[k2]
+        N = c.N
+        m1 = np.arange(N)[None, :] * np.ones((N, 1), dtype=np.int64)
+        m2 = np.arange(N)[:, None] * np.ones((1, N), dtype=np.int64)
+        diag = (m1 - m2 + N - 1) if slip == "G_diagonal_difference" else (m1 + m2)
+        ax_e, ax_f = (0, 1) if slip == "E_F_axes_swapped" else (1, 0)
+        res = []
+        for k3, t in gates:
+            isl = dict(k3=k3, npts=int((t > 0).sum()), D=0.0, E=0.0, F=0.0, G=0.0, H=0.0)
+            tD = (t > 0).astype(np.float64) if slip == "D_without_edge_weight" else t
+            isl["D"] = float(np.sum(tD * np.abs(Y) ** 2) * d1 * d2)
+            if k3 == k1 and "E" in need:
+                r = np.sum(t * Y, axis=ax_e) * d1
+                isl["E"] = float(np.sum(np.abs(r) ** 2) * d2)
+            if k3 == k2 and "F" in need:
+                col = np.sum(t * Y, axis=ax_f) * d2
+                isl["F"] = float(np.sum(np.abs(col) ** 2) * d1)
+            if k1 == k2 and "G" in need:
+                G = 0.0
+                for d in range(2 * N - 1):
+                    on = (diag == d) & (t > 0)
+                    if not on.any():
+                        continue
+                    G += t[on][0] * abs(np.sum(Y[on]) * d1) ** 2 * d1
+                isl["G"] = float(G)
+            if k1 == k2 == k3 and "H" in need:
+                tH = 1.0 if slip == "H_without_gate" else t
+                isl["H"] = float(abs(np.sum(tH * Y) * d1 * d2) ** 2)
+            res.append(isl)
+        return res
+    return region_islands
+
+
+def _islands(slip):
+    def apply(fwm, isrs, link, egn):
+        egn.region_islands = _region_islands_with(slip)
+    return apply
+
+
+def _apply_eta_over_p_squared(fwm, isrs, link, egn):
+    orig = egn.eta
+
+    def eta(lk, coi=None, **kw):
+        e, t = orig(lk, coi=coi, **kw)[:2]
+        c = egn.canonicalize(lk)
+        idx = list(range(c.f.size)) if coi is None else list(coi)
+        s = c.P[idx]                                                 # slip: / P^2, not / P^3
+        return e * s, t * s[:, None]
+    egn.eta = eta
+
+
+MUTANTS.update({
+    "E_F_axes_swapped": _islands("E_F_axes_swapped"),
+    "G_diagonal_difference": _islands("G_diagonal_difference"),
+    "H_without_gate": _islands("H_without_gate"),
+    "D_without_edge_weight": _islands("D_without_edge_weight"),
+    "f3_plus_f": _islands("f3_plus_f"),
+    "eta_over_p_squared": _apply_eta_over_p_squared,
+})
+
+
 def apply(name):
     from oracle import egn, fwm, isrs, link
     MUTANTS[name](fwm, isrs, link, egn)

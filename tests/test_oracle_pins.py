@@ -280,6 +280,11 @@ def test_generalised_islands_reduce_to_eq16_when_spacing_equals_R():
         want = sorted((k1 + M, k2 + M, k1 + k2 - kappa + ll + M)
                       for k1, k2, ll in egn.island_set_eq16(M, kappa))
         assert got == want
+        # and the islands region_islands integrates are those same (k1, k2, k3)
+        c = egn.canonicalize(l)
+        integrated = sorted((k1, k2, isl["k3"]) for k1 in range(2 * M + 1) for k2 in range(2 * M + 1)
+                            for isl in egn.region_islands(c, kappa + M, k1, k2, "unit"))
+        assert integrated == want
 
 
 def test_P9_only_l0_islands_when_R_below_two_thirds_spacing():
@@ -339,6 +344,26 @@ def test_P6_unit_link_raw_integrals():
     assert abs(isl["H"] / R ** 4 - 9.0 / 16.0) < 1e-13
     for k in "EFG":
         assert abs(isl[k] / R ** 3 - 7.0 / 12.0) < 1e-5
+
+
+def test_P6_two_rate_unit_link_coherent_axes():
+    # C7 on a two-rate link with Y := 1 (geometry only): COI = the 32 GBd channel (R1), the other
+    # channel 64 GBd (R0).  Region (kappa=1, k1=0, k2=1): f3 = f1 + (f2 - f) stays in band 0, so
+    # the island is k3 = k1 (E gate); E is coherent over f1 at fixed f2:
+    #   E = int_{-R1/2}^{R1/2} (R0 - |u|)^2 du = 2/3 (R0^3 - (R0 - R1/2)^3),  D = R0 R1 - R1^2/4.
+    # Region (kappa=1, k1=1, k2=0) mirrors it with k3 = k2 (F gate), F coherent over f2 at fixed
+    # f1 takes the same value.  Summing over the other axis would give (R0 - R1) R1^2 + 2/3 R1^3.
+    R0, R1 = 64e9, 32e9
+    l = tiny_link(n_ch=2, rates_gbd=(64, 32), spacing_ghz=100.0, n_span=1, grid_n=64, fmts=("qpsk",))
+    c = egn.canonicalize(l)
+    coh = 2.0 / 3.0 * (R0 ** 3 - (R0 - R1 / 2) ** 3)
+    area = R0 * R1 - R1 ** 2 / 4
+    (isl_e,) = egn.region_islands(c, 1, 0, 1, "unit")
+    assert isl_e["k3"] == 0 and abs(isl_e["D"] / area - 1) < 1e-14
+    assert abs(isl_e["E"] / coh - 1) < 1e-4 and isl_e["F"] == 0.0
+    (isl_f,) = egn.region_islands(c, 1, 1, 0, "unit")
+    assert isl_f["k3"] == 0 and abs(isl_f["D"] / area - 1) < 1e-14
+    assert abs(isl_f["F"] / coh - 1) < 1e-4 and isl_f["E"] == 0.0
 
 
 def test_P14_unit_link_3d_D_exact_discrete():
