@@ -16,7 +16,9 @@
  * number of Hz, and symbol_rate_hz / (2 * grid_n) is an integer, so that every grid frequency
  * and every f1 + f2 - f is exact in fp64 and band-edge ties are decided exactly.
  *
- * Threading: a handle is not thread-safe; distinct handles are independent.
+ * Threading: a handle is not thread-safe; distinct handles are independent.  Successive calls on
+ * one handle are ordered on the device even when issued on different streams (a call on a new
+ * stream waits for the previous call's end on the device, not on the host).
  * Errors: every call returns a status; on error nothing is enqueued and outputs are untouched;
  * isrs_egn_last_error() (thread-local) names the offending field / index.
  */

@@ -743,6 +743,9 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
         cudaEventCreate(&h->evc[0]) != cudaSuccess || cudaEventCreate(&h->evc[1]) != cudaSuccess)
       return cuda_fail(cudaGetLastError(), "side stream / events");
   }
+  // calls on one handle share its partials: a call on another stream than the previous one waits
+  // (on the device) for the previous call's end, so successive calls stay ordered
+  if (h->have_result && st != h->last_stream) cudaStreamWaitEvent(st, h->ev[3], 0);
   // fork: the coherent regions run on the side stream while the D-only regions run on `st`;
   // join before the per-COI reduce.  ev[0] -> ev[2] brackets the whole integrand phase.
   cudaEventRecord(h->ev[0], st);

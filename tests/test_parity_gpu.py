@@ -457,6 +457,25 @@ def test_fp32_variant_vs_fp64_full_size(isrs, cfg, coi):
     assert np.all(d <= DB_TOL_FP32), (cfg, d.max())
 
 
+def test_streams_one_handle_and_two_handles(isrs):
+    """Successive calls on one handle issued on different streams stay ordered on the device, and
+    two handles run concurrently on two streams: every result equals its single-stream eta bitwise."""
+    l1 = bj_config("c1")
+    l2 = tiny_link(**TINY["mixed_rates_guard"])
+    ref1, _ = gpu_eta(isrs, l1)
+    ref2, _ = gpu_eta(isrs, l2)
+    s = [torch.cuda.Stream() for _ in range(3)]
+    with isrs.Engine(l1) as e1, isrs.Engine(l2) as e2:
+        outs = []
+        for i in range(6):
+            outs.append((e1.nli(stream=s[i % 3]), e2.nli(stream=s[(i + 1) % 3]), e1.nli(coi=[0, 4], stream=s[(i + 2) % 3])))
+        torch.cuda.synchronize()
+        for a, b, c in outs:
+            assert np.array_equal(a.cpu().numpy(), ref1)
+            assert np.array_equal(b.cpu().numpy(), ref2)
+            assert np.array_equal(c.cpu().numpy(), ref1[[0, 4]])
+
+
 def test_full_size_determinism_c2(isrs):
     link = bj_config("c2")
     with isrs.Engine(link) as e:
