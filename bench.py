@@ -144,10 +144,6 @@ def dist_setup(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if ws > 1:
-        import torch.distributed as dist
-        backend = args.backend or ("nccl" if args.impl == "ours" else "gloo")
-        dist.init_process_group(backend)
     if args.impl == "ours":
         import torch
         ndev = torch.cuda.device_count()
@@ -155,6 +151,16 @@ def dist_setup(args):
             # more ranks than GPUs (functional test of the multi-rank path only; the driver runs
             # one rank per GPU): ranks share devices round-robin
             local = local % ndev
+        if ndev:
+            torch.cuda.set_device(local)     # before NCCL init: barriers / comms bind to this GPU
+    if ws > 1:
+        import torch.distributed as dist
+        backend = args.backend or ("nccl" if args.impl == "ours" else "gloo")
+        if backend == "nccl":
+            import torch
+            dist.init_process_group(backend, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return ws, rank, local
 
 
