@@ -1,7 +1,7 @@
 """Time the oracle (oracle/, numpy fp64, closed mode = literal Eqs. 8-10) on whole small configs and
 on bounded samples of the large ones, on this host's cores (SURVEY.md §8(d) "oracle timed beside it").
 
-    python tools/oracle_timing.py [--configs c1] [--sample c2,c3,c4,c5] [--seconds 20]
+    python tests/tools/oracle_timing.py [--configs c1] [--sample c2,c3,c4,c5] [--seconds 20]
 
 One JSON line per config: point-spans, seconds, point-spans/s, processes used.
 """
@@ -11,7 +11,7 @@ import os
 import sys
 import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 
