@@ -5,8 +5,9 @@ computes: the ISRS EGN NLI coefficient eta(f_COI) with the segment closed-form F
 efficiency factor (Eqs. 7-10), plus the integral form (Eq. 23, `quad` mode) and
 the Maclaurin closed form (Eq. 4) used as pins and for the NEXT rows.
 
-Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s cpu_baseline / `--impl reference`
-legs may import anything under `oracle/`.  The product package
+Only `tests/` (including the whole-eta parity and oracle-timing scripts in `tests/tools/`),
+`__graft_entry__.smoke()` and `bench.py`'s cpu_baseline / `--impl reference` legs may import
+anything under `oracle/`.  The product package
 `paper_2412_11614_b200/` never imports it, and this package never imports the product:
 the two share no code.  The only shared module is `workloads/` (seeded inputs, no method
 arithmetic).
@@ -25,5 +26,6 @@ Modules
              the 3-D form over the COI band (NEXT-3 / R10)
 
 Parity status: every function is pinned by a `-m "not gpu"` test in tests/test_oracle_*.py
-except where its docstring says "parity unpinned" (DESIGN.md lists those).
+except where its docstring says "parity unpinned" (DESIGN.md lists those); tests/test_oracle_mutants.py
+plants 28 plausible slips in these modules one at a time and checks that the pins catch each.
 """
