@@ -41,3 +41,25 @@ def test_product_arm_fails_loudly_without_gpu():
     r = _run(["--steps", "1", "--warmup", "1", "--no-cpu", "--no-e2e", "--no-dedup"])
     assert r.returncode != 0
     assert not [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+
+
+def test_roofline_unit_counts():
+    # a chain of G spans with K segments (K_p = K rounded up to even) costs
+    # 3 (G K_p - 1) + 40 flops and 2 (G K_p - 1) + 25 FP64 slots per point
+    sys.path.insert(0, ROOT)
+    import bench
+    assert bench.algorithmic_work_per_point([10], [80] * 10) == (3 * 799 + 40, 2 * 799 + 25)
+    # odd K pads to even; unchained spans count one chain each
+    assert bench.algorithmic_work_per_point([1, 1], [73, 81]) == (3 * 73 + 40 + 3 * 81 + 40,
+                                                                  2 * 73 + 25 + 2 * 81 + 25)
+
+
+def test_traffic_source_is_the_newest_c2_capture():
+    sys.path.insert(0, ROOT)
+    import glob
+    import bench
+    traffic, src = bench.ncu_traffic()
+    caps = [os.path.basename(f).split("_")[0] for f in glob.glob(os.path.join(ROOT, "profiles", "*ncu_integrand*_c2*.json"))
+            if "fp32" not in f]
+    newest = max(caps, key=lambda t: (len(t), t))
+    assert src is not None and os.path.basename(src).startswith(newest + "_") and traffic > 0
