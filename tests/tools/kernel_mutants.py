@@ -1,0 +1,79 @@
+"""Are the GPU parity tests sharp?  Plant ONE slip in a copy of the CUDA sources (the tree itself is
+never touched), build the library from the copy, and run the fast GPU parity tests against it via
+ISRS_EGN_LIB: every mutant must fail them.
+
+    python tests/tools/kernel_mutants.py build          # here (nvcc cross-compiles): build_variants/lib_mut_*.so
+    python tests/tools/kernel_mutants.py run            # on the GPU box: one pytest run per mutant
+
+Prints one JSON line per mutant: name, slip, pytest exit code, killed (exit code 1).
+"""
+import json
+import os
+import shutil
+import subprocess
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+OUT = os.path.join(ROOT, "build_variants")
+
+# name: (file under paper_2412_11614_b200/csrc, exact original text, mutated text, what the slip is)
+MUTANTS = {
+    "goertzel_plus_b2": ("kernels.cu", "n0[q] = fma(c2[q], b1[q], tc.x) - b2[q];",
+                         "n0[q] = fma(c2[q], b1[q], tc.x) + b2[q];", "recurrence: + b_{k+2} in the even step"),
+    "walk_power_index": ("kernels.cu", "vr[m] = v * sp[m];", "vr[m] = v * sp[m > 0 ? m - 1 : 0];",
+                         "table walk: step^m off by one inside a run"),
+    "wrap_pair_missing": ("kernels.cu", "if (ii < 2) sm.T[r * p.tstride + Kp + ii] = x;",
+                          "if (ii < 1) sm.T[r * p.tstride + Kp + ii] = x;",
+                          "chain wrap: only one of the two wrapped coefficients"),
+    "I0_sign": ("kernels.cu", "const double wr1 = fma(Eh, cs[q], -1.0), wi = Eh * sn[q];",
+                "const double wr1 = fma(Eh, cs[q], -1.0), wi = -Eh * sn[q];", "I_0: conj(w) for w"),
+    "phase_one_span_short": ("kernels.cu", "double t2 = fma(x[q], (double)(Ks * G), th[q]);",
+                             "double t2 = fma(x[q], (double)(Ks * (G > 1 ? G - 1 : G)), th[q]);",
+                             "span phase: a chain advances theta by G-1 spans"),
+    "gate_edge_weight": ("kernels.cu", "const double t = (f3 > l && f3 < h) ? 1.0 : 0.5;",
+                         "const double t = (f3 > l && f3 < h) ? 1.0 : 1.0;", "C10: band-edge points weigh 1"),
+    "coherent_row_weight": ("kernels.cu", "acc.x = fma(w, y.x, acc.x);", "acc.x = fma(w, y.x, 0.5 * acc.x);",
+                            "E row sum: halves the running sum"),
+    "lattice_m2": ("kernels.cu", "const int m2f = (b == 1) ? lj - a * m1f : (lj - a * m1f) / b;",
+                   "const int m2f = (b == 1) ? lj - a * m1f : (lj - a * m1f) / b + (a > 1);",
+                   "point geometry: m2 off by one on mixed-rate lattices"),
+}
+
+FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
+         "-Xcompiler", "-fvisibility=hidden", "-shared", "--expt-relaxed-constexpr"]
+TESTS = "tiny or edge or random_links or c1_full or streams"
+
+
+def build():
+    os.makedirs(OUT, exist_ok=True)
+    for name, (fn, old, new, _) in MUTANTS.items():
+        with tempfile.TemporaryDirectory() as td:
+            src = os.path.join(td, "paper_2412_11614_b200", "csrc")
+            shutil.copytree(os.path.join(ROOT, "paper_2412_11614_b200", "csrc"), src)
+            shutil.copytree(os.path.join(ROOT, "include"), os.path.join(td, "include"))
+            path = os.path.join(src, fn)
+            text = open(path).read()
+            assert text.count(old) >= 1, f"{name}: pattern not found"
+            open(path, "w").write(text.replace(old, new, 1))
+            lib = os.path.join(OUT, f"lib_mut_{name}.so")
+            cmd = ["nvcc"] + FLAGS + ["-I", os.path.join(td, "include"), os.path.join(src, "abi.cu"),
+                                      os.path.join(src, "kernels.cu"), "-o", lib]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            print(name, "built" if r.returncode == 0 else r.stderr[-500:], flush=True)
+
+
+def run():
+    for name, (_, _, _, what) in MUTANTS.items():
+        lib = os.path.join(OUT, f"lib_mut_{name}.so")
+        env = dict(os.environ, ISRS_EGN_LIB=lib)
+        r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_parity_gpu.py"),
+                            "-m", "gpu", "-x", "-q", "-p", "no:cacheprovider", "-k", TESTS],
+                           cwd=ROOT, env=env, capture_output=True, text=True, timeout=1800)
+        tail = [l for l in r.stdout.splitlines() if "passed" in l or "failed" in l]
+        print(json.dumps({"mutant": name, "slip": what, "pytest_rc": r.returncode, "killed": r.returncode == 1,
+                          "summary": tail[-1] if tail else r.stdout[-300:]}), flush=True)
+
+
+if __name__ == "__main__":
+    {"build": build, "run": run}[sys.argv[1]]()
