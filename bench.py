@@ -220,7 +220,9 @@ def run_reference(args, link, ws, rank):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
             "steps": steps, "warmup": warm, "ms_per_step": 1e3 * float(np.mean(per_step)),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": config_desc(link, args),
+            "data": "synthetic",
+            "config": dict(config_desc(link, args), l2="n/a (host CPU oracle)",
+                           parallelism=f"{cores} host processes (oracle, closed mode)"),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": desc + " per step"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
