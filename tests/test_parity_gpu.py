@@ -476,6 +476,21 @@ def test_streams_one_handle_and_two_handles(isrs):
             assert np.array_equal(c.cpu().numpy(), ref1[[0, 4]])
 
 
+def test_graph_replay_equals_nli(isrs):
+    """Engine.graph(): the captured call (fork, both integrand launches, join, reduce) replays to the
+    same eta and D..H bitwise, repeatedly, for c1 and a multi-class tiny link with a COI subset."""
+    for link, coi in ((bj_config("c1"), None), (tiny_link(**TINY["random_spans_multiclass"]), [2, 0])):
+        ref, tref = gpu_eta(isrs, link, coi=coi)
+        with isrs.Engine(link) as e:
+            g = e.graph(coi=coi, terms=True)
+            for _ in range(3):
+                g.eta.zero_()
+                eta, terms = g.replay()
+                torch.cuda.synchronize()
+                assert np.array_equal(eta.cpu().numpy(), ref)
+                assert np.array_equal(terms.cpu().numpy(), tref)
+
+
 def test_full_size_determinism_c2(isrs):
     link = bj_config("c2")
     with isrs.Engine(link) as e:
