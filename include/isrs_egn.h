@@ -21,6 +21,9 @@
  * stream waits for the previous call's end on the device, not on the host).
  * Errors: every call returns a status; on error nothing is enqueued and outputs are untouched;
  * isrs_egn_last_error() (thread-local) names the offending field / index.
+ * CUDA graphs: once a handle has run a COI set on a stream, a further isrs_egn_nli for the same COI
+ * set on that stream neither allocates nor synchronises the host, so it can be captured with
+ * cudaStreamBeginCapture and replayed (the Python Engine.graph() does exactly this).
  * Memory: a handle's device buffers come from the device's default stream-ordered memory pool
  * (cudaMallocAsync), whose release threshold the library raises so that repeated create / destroy
  * reuse pool memory; memory a destroyed handle frees stays reserved in that pool for the process.
