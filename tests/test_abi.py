@@ -109,6 +109,8 @@ def test_validation_errors_before_any_cuda(abi):
     assert rc == abi.EINVAL and "cr_per_w_m_hz[1]" in msg
     rc, msg, _ = _create(abi, l, grid_n=8192)
     assert rc == abi.EINVAL and "4096" in msg
+    rc, msg, _ = _create(abi, l, dz=1e-3)               # K_s = 8e7 segments
+    assert rc == abi.ERANGE and "K_s" in msg
 
 
 def test_destroy_null_safe(abi):

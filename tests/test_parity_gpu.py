@@ -240,6 +240,9 @@ def test_errors_surface_from_nli(isrs):
     with isrs.Engine(link) as e:
         with pytest.raises(isrs.IsrsEgnError):
             e.nli(coi=[3])
+    # K_s = 8000 segments (dz = 10 m) leaves no room for two envelope-table rows in shared memory
+    with pytest.raises(isrs.IsrsEgnError, match="shared-memory"):
+        isrs.Engine(link, delta_z_m=10.0)
 
 
 # ------------------------------------------------------------------ full BASELINE sizes
