@@ -4,8 +4,11 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
 
 One step = one pass of the whole hot path (rows a2-a7: the nli() call: integrand kernels over
-every region of every COI + per-COI assembly) over BASELINE.json configs[1] (c2: C-band 40 x
-64 GBd, 10 x 80 km, N = 128, all 40 channels as COI), inputs resident in HBM.  At N GPUs
+every region of every requested COI + per-COI assembly), inputs resident in HBM.  The default
+workload is BASELINE.json configs[4] (c5: S+C+L 20 THz, 200 x 96 GBd, 50 x 80 km, N = 256 -- the
+north-star link) on the COI subset {0, 100, 199} that SURVEY.md 8(d) prescribes for c3-c5
+(lowest, centre, highest channel; ~2.5 s per step); `--config c2 --coi all` is round 1's
+C-band headline, and c2 (all COIs) and c4 ({0, 40, 79}) are timed as extra keys.  At N GPUs
 (torchrun, one process per GPU) the canonical region list is split into N cost-balanced
 contiguous shards; each rank evaluates its shard, the per-COI sums (n_ch x 6 fp64) are
 all-gathered over NCCL and combined in fixed rank order: strong scaling of one
@@ -57,9 +60,22 @@ def algorithmic_work_per_point(chain_g, k_s):
     return flops, slots
 
 
-def ncu_traffic():
+DEFAULT_COI = {"c3": [0, 50, 99], "c4": [0, 40, 79], "c5": [0, 100, 199]}
+
+
+def parse_coi(spec, link):
+    """--coi: 'all' -> None (every channel), 'default' -> SURVEY 8(d)'s {0, n/2, n-1} subset for
+    c3-c5 (all channels for c1, c2), else a comma-separated list."""
+    if spec == "all":
+        return None
+    if spec == "default":
+        return DEFAULT_COI.get(link.name)
+    return [int(x) for x in spec.split(",")]
+
+
+def ncu_traffic(config="c5"):
     """DRAM bytes (read + write) per launch of the D-only integrand kernel from the newest committed
-    `ncu --set full` summary under profiles/ (tools/ncu_summary.py), or (None, None)."""
+    `ncu --set full` summary of `config` under profiles/ (tools/ncu_summary.py), or (None, None)."""
     import glob
     best = None
     def order(fn):            # r01a < ... < r01z < r01aa < r01ab: by tag length, then name
@@ -67,7 +83,7 @@ def ncu_traffic():
         return (len(tag), tag)
 
     for fn in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_integrand*.json")), key=order):
-        if "fp32" in fn or "_c2" not in fn:   # the bench config's capture only
+        if "fp32" in fn or f"_{config}" not in fn:   # the bench config's capture only
             continue
         try:
             with open(fn) as fh:
@@ -172,25 +188,26 @@ def _oracle_region(args):
     return npts * link.n_span
 
 
-def oracle_regions(link):
-    """Canonical (kappa, k1, k2) regions with support of the middle COI, spread evenly (the CPU
-    sample is a stride through them so it covers short edge regions and long centre ones)."""
+def oracle_regions(link, coi=None):
+    """Canonical (kappa, k1, k2) regions with support of the requested COIs (all channels when
+    None), in canonical order (COI, k1, k2); the CPU sample is a stride through them so it covers
+    short edge regions and long centre ones of every COI."""
     from oracle import egn
     c = egn.canonicalize(link)
-    mid = link.n_ch // 2
-    return [(mid, k1, k2) for k1 in range(link.n_ch) for k2 in range(link.n_ch)
-            if egn.has_support_bound(c, mid, k1, k2)]
+    cois = list(range(link.n_ch)) if coi is None else list(coi)
+    return [(k, k1, k2) for k in cois for k1 in range(link.n_ch) for k2 in range(link.n_ch)
+            if egn.has_support_bound(c, k, k1, k2)]
 
 
-def oracle_sample(link, seconds_target, cores=None):
+def oracle_sample(link, seconds_target, coi=None, cores=None):
     """Time the oracle as it stands (numpy fp64, closed mode) on a bounded sample of the
     workload's regions, one process per host core.  Returns (point-spans/s, point-spans,
     seconds, cores, sample description)."""
     import multiprocessing as mp
     cores = cores or os.cpu_count() or 1
-    regs = oracle_regions(link)
+    regs = oracle_regions(link, coi)
     t0 = time.perf_counter()
-    _oracle_region((link, regs[len(regs) // 2]))           # calibrate: one centre region
+    _oracle_region((link, regs[len(regs) // 2]))           # calibrate: one mid-list region
     t1 = max(time.perf_counter() - t0, 1e-3)
     m = int(min(len(regs), max(cores, round(seconds_target * cores / t1))))
     stride = max(1, len(regs) // m)
@@ -200,28 +217,31 @@ def oracle_sample(link, seconds_target, cores=None):
         t0 = time.perf_counter()
         pspans = sum(pool.map(_oracle_region, [(link, r) for r in sample], chunksize=1))
         dt = time.perf_counter() - t0
+    which = "every COI" if coi is None else f"COIs {list(coi)}"
     desc = (f"oracle closed mode (numpy fp64, {cores} processes) on {len(sample)} of the {len(regs)} "
-            f"regions of COI {link.n_ch // 2} of {link.name} (every {stride}th, canonical order)")
+            f"regions of {which} of {link.name} (every {stride}th, canonical order)")
     return pspans / dt, pspans, dt, cores, desc
 
 
-def run_reference(args, link, ws, rank):
+def run_reference(args, link, coi, ws, rank):
     if rank != 0:
         return
     steps, warm = args.steps, args.warmup
     per_step = []
     pspans_tot = 0
     for i in range(warm + steps):
-        rate, ps, dt, cores, desc = oracle_sample(link, args.ref_seconds)
+        rate, ps, dt, cores, desc = oracle_sample(link, args.ref_seconds, coi)
         if i >= warm:
             per_step.append(dt)
             pspans_tot += ps
     value = pspans_tot / sum(per_step)
+    cfg = config_desc(link, coi, args)
+    cfg["workload"] += "; each step a bounded region sample of it (see cpu_baseline.sample)"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
             "steps": steps, "warmup": warm, "ms_per_step": 1e3 * float(np.mean(per_step)),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": dict(config_desc(link, args), l2="n/a (host CPU oracle)",
+            "config": dict(cfg, l2="n/a (host CPU oracle)",
                            parallelism=f"{cores} host processes (oracle, closed mode)"),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": desc + " per step"},
@@ -229,11 +249,16 @@ def run_reference(args, link, ws, rank):
     print(json.dumps(line), flush=True)
 
 
-def config_desc(link, args):
+def coi_text(link, coi):
+    return "all channels as COI" if coi is None else f"COIs {','.join(str(c) for c in coi)}"
+
+
+def config_desc(link, coi, args):
     return {"workload": f"{link.name}: {link.n_ch} ch x {int(link.symbol_rate_hz[0] / 1e9)} GBd, "
-                        f"{link.n_span} spans, N={link.grid_n}, dz={link.delta_z_m:g} m, all channels as COI",
+                        f"{link.n_span} spans, N={link.grid_n}, dz={link.delta_z_m:g} m, {coi_text(link, coi)}",
             "n_ch": link.n_ch, "n_span": link.n_span, "grid_n": link.grid_n,
-            "n_coi": link.n_ch, "seed": link.seed,
+            "n_coi": link.n_ch if coi is None else len(coi), "coi": "all" if coi is None else list(coi),
+            "seed": link.seed,
             "l2": "flushed between timed steps (256 MiB write, outside the step events)",
             "parallelism": (f"region shards x{args.gpus} (cost-balanced contiguous shards of one link, "
                             f"{(args.backend or 'nccl').upper()} all-gather of per-COI sums, fixed-order combine; "
@@ -241,14 +266,105 @@ def config_desc(link, args):
                             if args.gpus > 1 else "1 GPU")}
 
 
-def run_ours(args, link, ws, rank, local):
+def roofline_of(eng, link, kern_ms, precision):
+    """Roofline of the dominant kernel: the integrand phase (D-only launch + the concurrent coherent
+    launch on the library's side stream, fork to join; CUDA events inside the library, on the
+    launching streams), algorithmic flops per point-span x point-spans / time."""
+    ki_ms = float(np.mean([k[0][3] for k in kern_ms]))
+    ps_i = kern_ms[-1][1][2]
+    chain_g, k_s = eng.span_chains()
+    fpp, spp = (v / link.n_span for v in algorithmic_work_per_point(chain_g, k_s))  # per point-span
+    ach = ps_i * fpp / (ki_ms * 1e-3) / 1e12
+    # fp64: 64 FP64 FMA lanes per SM; the mixed fp32 variant (a8) runs its recurrence on the
+    # 128 FP32 FMA lanes per SM, so its roofline takes the FP32 peak (2x)
+    peak = fp64_peak_tflops() * (2.0 if precision == 32 else 1.0)
+    slots_ach = ps_i * spp / (ki_ms * 1e-3) / 1e12
+    slots_peak = SMS * FP64_LANES * SM_MAX_MHZ * 1e6 / 1e12
+    return dict(ki_ms=ki_ms, ps_i=ps_i, chain_g=chain_g, k_s=k_s, fpp=fpp, spp=spp, ach=ach, peak=peak,
+                slots_ach=slots_ach, slots_peak=slots_peak)
+
+
+def time_steps(eng, step, stream, flush, steps, warmup, barrier=None, clocks=None):
+    """W untimed warm-up steps, then `steps` steps each bracketed by CUDA events on `stream` (the
+    L2 flush sits outside the events); returns (ms per step list, library kernel times list, clocks)."""
+    import torch
+    with torch.cuda.stream(stream):
+        for _ in range(warmup):
+            flush.zero_()
+            step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    kern_ms = []
+    if barrier:
+        barrier()
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
+    with torch.cuda.stream(stream):
+        for k in range(steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+            kern_ms.append(eng.last_kernel_ms())          # events inside the library, same stream
+    torch.cuda.synchronize()
+    clk = clocks.stop() if clocks else None
+    if barrier:
+        barrier()
+    return [a.elapsed_time(b) for a, b in ev], kern_ms, clk
+
+
+def e2e_host(isrs, link, coi, device, precision, reps):
+    """End to end through the public API with HOST buffers (isrs_egn_eta_host: validate + region
+    plan + H2D + precompute + nli + D2H + free), wall clock, one warm-up call; returns seconds."""
+    isrs.eta_host(link, coi=coi, device=device, precision=precision)
+    t = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        isrs.eta_host(link, coi=coi, device=device, precision=precision)
+        t.append(time.perf_counter() - t0)
+    return t
+
+
+def extra_config(isrs, name, spec, args, local, stream, flush):
+    """One more BASELINE config timed like the headline (fewer steps) and reported as an extra key."""
+    import torch
+    from workloads import bj_config
+    link = bj_config(name)
+    coi = parse_coi(spec, link)
+    n = link.n_ch if coi is None else len(coi)
+    dev = torch.device("cuda", local)
+    eta = torch.empty(n, dtype=torch.float64, device=dev)
+    with isrs.Engine(link, device=local, precision=args.precision) as eng:
+        cp = coi
+
+        def step():
+            eng.nli_into(eta.data_ptr(), 0, cp, stream.cuda_stream)
+        step_ms, kern_ms, _ = time_steps(eng, step, stream, flush, 5, 3)
+        pts, pspans, nreg = eng.work()
+        rf = roofline_of(eng, link, kern_ms, args.precision)
+    ms = float(np.mean(step_ms))
+    out = {"workload": f"{name}: {coi_text(link, coi)}", "value": pspans / (ms * 1e-3), "unit": UNIT,
+           "ms_per_step": ms, "steps": 5, "warmup": 3, "point_spans_per_step": pspans,
+           "channels_per_s": n / (ms * 1e-3), "roofline_frac": rf["ach"] / rf["peak"],
+           "integrand_phase_ms": rf["ki_ms"]}
+    if not args.no_e2e:
+        t = e2e_host(isrs, link, coi, local, args.precision, 3)
+        out["e2e"] = {"value": pspans / float(np.median(t)), "unit": UNIT,
+                      "samples_ms": [round(1e3 * x, 2) for x in t]}
+    return out
+
+
+def run_ours(args, link, coi, ws, rank, local):
     import torch
     import paper_2412_11614_b200 as isrs
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(device=dev)
     eng = isrs.Engine(link, device=local, precision=args.precision)
-    n = link.n_ch
+    n = link.n_ch if coi is None else len(coi)
     eta = torch.empty(n, dtype=torch.float64, device=dev)
     terms = torch.empty((n, 5), dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -262,48 +378,29 @@ def run_ours(args, link, ws, rank, local):
         gathered = torch.empty(ws * n * 6, dtype=torch.float64, device=dev)
 
         def step():
-            eng.nli_shard_into(rank, ws, sums.data_ptr(), None, stream.cuda_stream)
+            eng.nli_shard_into(rank, ws, sums.data_ptr(), coi, stream.cuda_stream)
             dist.all_gather_into_tensor(gathered, sums)
-            eng.combine_into(ws, gathered.data_ptr(), eta.data_ptr(), terms.data_ptr(), None,
+            eng.combine_into(ws, gathered.data_ptr(), eta.data_ptr(), terms.data_ptr(), coi,
                              stream.cuda_stream)
+        barrier = torch.distributed.barrier
     else:
         def step():
-            eng.nli_into(eta.data_ptr(), terms.data_ptr(), None, stream.cuda_stream)
+            eng.nli_into(eta.data_ptr(), terms.data_ptr(), coi, stream.cuda_stream)
+        barrier = None
 
+    # one untimed call so the work list exists, then the work counts of this rank's share
     with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            flush.zero_()
-            step()
+        step()
     torch.cuda.synchronize()
-    pts, pspans, nreg = eng.work()          # this rank's share
+    pts, pspans, nreg = eng.work()
     launches_per_step = eng.last_launch_count() + (1 if ws > 1 else 0)
     if ws > 1:
         tot = torch.tensor([pts, pspans, nreg], dtype=torch.int64, device=dev)
         torch.distributed.all_reduce(tot)
         pts, pspans, nreg = (int(v) for v in tot.tolist())
 
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    kern_ms = []
-    if ws > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
-    with torch.cuda.stream(stream):
-        for k in range(args.steps):
-            flush.zero_()
-            ev[k][0].record(stream)
-            step()
-            ev[k][1].record(stream)
-            kms, kps = eng.last_kernel_ms()          # events inside the library, same stream
-            kern_ms.append((kms, kps))
-    torch.cuda.synchronize()
-    clk = clocks.stop()
-    if ws > 1:
-        torch.distributed.barrier()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
+    step_ms, kern_ms, clk = time_steps(eng, step, stream, flush, args.steps, args.warmup, barrier,
+                                       ClockSampler(local))
     ms = float(np.mean(step_ms))
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if ws > 1:
@@ -317,48 +414,34 @@ def run_ours(args, link, ws, rank, local):
         ge = ge.cpu().numpy().reshape(ws, n)
         same_eta = bool(all(np.array_equal(ge[0], ge[r]) for r in range(ws)))
 
-    # roofline of the dominant kernel: the integrand phase (D-only launch + the concurrent
-    # coherent launch on the library's side stream, fork to join; CUDA events inside the library)
     kd_ms = float(np.mean([k[0][0] for k in kern_ms]))
     kc_ms = float(np.mean([k[0][1] for k in kern_ms]))
     kr_ms = float(np.mean([k[0][2] for k in kern_ms]))
-    ki_ms = float(np.mean([k[0][3] for k in kern_ms]))
-    ps_i = kern_ms[-1][1][2]
-    chain_g, k_s = eng.span_chains()
-    fpp, spp = (v / link.n_span for v in algorithmic_work_per_point(chain_g, k_s))  # per point-span
-    ach = ps_i * fpp / (ki_ms * 1e-3) / 1e12
-    # fp64: 64 FP64 FMA lanes per SM; the mixed fp32 variant (a8) runs its recurrence on the
-    # 128 FP32 FMA lanes per SM, so its roofline takes the FP32 peak (2x)
-    peak = fp64_peak_tflops() * (2.0 if args.precision == 32 else 1.0)
-    slots_ach = ps_i * spp / (ki_ms * 1e-3) / 1e12
-    traffic, traffic_src = ncu_traffic()
-    survey_fpp = float(np.mean(8 * np.asarray(k_s, dtype=float) + 100))     # 8 K_s + ~100
-    slots_peak = SMS * FP64_LANES * SM_MAX_MHZ * 1e6 / 1e12
+    rf = roofline_of(eng, link, kern_ms, args.precision)
+    traffic, traffic_src = ncu_traffic(link.name)
+    survey_fpp = float(np.mean(8 * np.asarray(rf["k_s"], dtype=float) + 100))     # 8 K_s + ~100
 
     # end to end through the public API with host buffers: create + nli + D2H + destroy
     e2e = None
     if not args.no_e2e:
         pa = isrs.ProblemArrays(link)
-        h2d = pa.nbytes()
-        t_e2e = []
+        h2d = pa.nbytes() + (0 if coi is None else 4 * len(coi))
+        reps = max(1, min(5, args.steps))
         if ws == 1:
-            isrs.eta_host(link, device=local, precision=args.precision)     # warm-up (one-time costs)
-        for k in range(max(1, min(7, args.steps))):
-            if ws > 1:
+            t_e2e = e2e_host(isrs, link, coi, local, args.precision, reps)
+        else:
+            t_e2e = []
+            for k in range(reps):
                 torch.distributed.barrier()
-            t0 = time.perf_counter()
-            if ws > 1:
+                t0 = time.perf_counter()
                 with isrs.Engine(link, device=local, precision=args.precision) as e2:
-                    s2 = e2.nli_shard(rank, ws).reshape(-1)
+                    s2 = e2.nli_shard(rank, ws, coi=coi).reshape(-1)
                     g2 = torch.empty(ws * n * 6, dtype=torch.float64, device=dev)
                     torch.distributed.all_gather_into_tensor(g2, s2)
-                    e2.combine(g2.reshape(ws, n, 6)).cpu()
-            else:
-                isrs.eta_host(link, device=local, precision=args.precision)
-            dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-            if ws > 1:
+                    e2.combine(g2.reshape(ws, n, 6), coi=coi).cpu()
+                dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
                 torch.distributed.all_reduce(dt, op=torch.distributed.ReduceOp.MAX)
-            t_e2e.append(float(dt.item()))
+                t_e2e.append(float(dt.item()))
         e2e = {"value": pspans / float(np.median(t_e2e)), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 8 * n, "samples_ms": [round(1e3 * x, 2) for x in t_e2e],
                "note": ("isrs_egn_eta_host(): validate + region plan + H2D + precompute + nli + D2H + free"
@@ -370,67 +453,66 @@ def run_ours(args, link, ws, rank, local):
     dedup = None
     if ws == 1 and not args.no_dedup:
         with isrs.Engine(link, device=local, precision=64, flags=isrs.FLAG_DEDUP) as ed:
-            with torch.cuda.stream(stream):
-                for _ in range(2):
-                    ed.nli_into(eta.data_ptr(), 0, None, stream.cuda_stream)
-                dms = []
-                for _ in range(3):
-                    flush.zero_()
-                    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    a0.record(stream)
-                    ed.nli_into(eta.data_ptr(), 0, None, stream.cuda_stream)
-                    a1.record(stream)
-                    torch.cuda.synchronize()
-                    dms.append(a0.elapsed_time(a1))
+            dms, _, _ = time_steps(ed, lambda: ed.nli_into(eta.data_ptr(), 0, coi, stream.cuda_stream),
+                                   stream, flush, 3, 2)
         dm = float(np.median(dms))
         dedup = {"value": pspans / (dm * 1e-3), "unit": UNIT + " (logical)", "ms_per_step": dm,
                  "note": "ISRS_EGN_FLAG_DEDUP: one K-segment sum per run of identical spans x the "
                          "phased-array factor; same eta (<= 1e-10), not the headline"}
 
+    extras = {}
+    if ws == 1 and not args.no_extra:
+        for name, spec in (("c2", "all"), ("c4", "default")):
+            if name != link.name:
+                extras[name] = extra_config(isrs, name, spec, args, local, stream, flush)
+
     if rank == 0:
-        value = pspans / (ms_max * 1e-3)          # the whole link's point-spans over all ranks
+        value = pspans / (ms_max * 1e-3)          # the whole workload's point-spans over all ranks
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None,
                 "dtype": "f64" if args.precision == 64 else "f32 (mixed, row a8)", "data": "synthetic",
-                "config": config_desc(link, args),
+                "config": config_desc(link, coi, args),
                 "channels_per_s": n / (ms_max * 1e-3),
                 "point_spans_per_step": pspans, "points_per_step": pts, "regions_per_step": nreg,
                 "kernel_ms": {"integrand_D": kd_ms, "integrand_coherent": kc_ms, "reduce": kr_ms,
-                              "integrand_phase": ki_ms,
+                              "integrand_phase": rf["ki_ms"],
                               "note": "coherent launch runs concurrently on a side stream"},
-                "roofline": {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                             "frac": ach / peak, "traffic": traffic, "traffic_source": traffic_src,
+                "roofline": {"bound": "alu", "achieved": rf["ach"], "peak": rf["peak"], "unit": "TFLOP/s",
+                             "frac": rf["ach"] / rf["peak"], "traffic": traffic, "traffic_source": traffic_src,
                              "kernel": "isrs::integrand_kernel<false,0> + <true,0> (D-only and coherent "
                                        "regions, concurrent; fork to join)",
-                             "flops_per_point_span": fpp,
-                             "span_chains": [int(g) for g in chain_g],
+                             "flops_per_point_span": rf["fpp"],
+                             "span_chains": [int(g) for g in rf["chain_g"]],
                              "peak_note": ("derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz "
                                            "(tools/dmma_probe.cu: a DFMA stream reaches 128 flop/SM-cycle = this peak)"
                                            if args.precision == 64 else
                                            "derived FP32 peak: 148 SM x 128 FP32 FMA/clk x 2 x 1965 MHz (the "
                                            "variant's recurrence is fp32; chi h, phase and Y stay fp64)")},
                 "survey_units": {"flops_per_point_span": survey_fpp,
-                                 "achieved": ps_i * survey_fpp / (ki_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
-                                 "frac": ps_i * survey_fpp / (ki_ms * 1e-3) / 1e12 / peak,
+                                 "achieved": rf["ps_i"] * survey_fpp / (rf["ki_ms"] * 1e-3) / 1e12,
+                                 "unit": "TFLOP/s",
+                                 "frac": rf["ps_i"] * survey_fpp / (rf["ki_ms"] * 1e-3) / 1e12 / rf["peak"],
                                  "note": "SURVEY.md 8(d) per-unit figure 8 K + 100 assumes a complex Horner "
                                          "step (8 flops per segment); this kernel's real second-order "
                                          "recurrence needs 3, so this ratio exceeds 1 and is not the "
                                          "roofline - `roofline` counts the flops the kernel's method needs"},
-                "fp64_pipe_slots": {"achieved": slots_ach, "peak": slots_peak, "unit": "T slot/s",
-                                    "frac": slots_ach / slots_peak, "per_point_span": spp,
+                "fp64_pipe_slots": {"achieved": rf["slots_ach"], "peak": rf["slots_peak"], "unit": "T slot/s",
+                                    "frac": rf["slots_ach"] / rf["slots_peak"], "per_point_span": rf["spp"],
                                     "note": "same algorithmic count with DFMA and DADD one FP64 "
                                             "pipe issue slot each (the recurrence's real bound)"},
-                "pct_fp64_peak": 100.0 * ach / peak,
+                "pct_fp64_peak": 100.0 * rf["ach"] / rf["peak"],
                 "gpu_launches": launches_per_step * args.steps,
                 "clocks": clk, "e2e": e2e,
-                "eta_db_first_mid_last": [float(10 * np.log10(eta_host[i])) for i in (0, n // 2, n - 1)]}
+                "eta_db": [float(10 * np.log10(x)) for x in (eta_host if n <= 8 else eta_host[[0, n // 2, n - 1]])]}
         if same_eta is not None:
             line["eta_bitwise_equal_across_ranks"] = same_eta
         if dedup is not None:
             line["dedup_effective"] = dedup
+        if extras:
+            line["other_configs"] = extras
         if not args.no_cpu and ws == 1:
-            rate, ps, dt, cores, desc = oracle_sample(link, args.cpu_seconds)
+            rate, ps, dt, cores, desc = oracle_sample(link, args.cpu_seconds, coi)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                                     "sample": f"{desc}; {ps} point-spans in {dt:.1f} s"}
         print(json.dumps(line), flush=True)
@@ -442,7 +524,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--coi", default="default",
+                    help="'default' (c3-c5: SURVEY 8(d)'s {0, n/2, n-1}; c1, c2: all), 'all', or a list")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32],
                     help="64: the fp64 hot path (default); 32: the mixed fp32 variant (row a8)")
@@ -450,16 +534,18 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dedup", action="store_true", help="skip the separate NEXT-4a dedup timing")
+    ap.add_argument("--no-extra", action="store_true", help="skip the extra c2 / c4 timings")
     ap.add_argument("--ref-seconds", type=float, default=8.0, help="CPU seconds per reference step")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU seconds of the cpu_baseline")
     args = ap.parse_args()
     from workloads import bj_config
     link = bj_config(args.config)
+    coi = parse_coi(args.coi, link)
     ws, rank, local = dist_setup(args)
     if args.impl == "reference":
-        run_reference(args, link, ws, rank)
+        run_reference(args, link, coi, ws, rank)
     else:
-        run_ours(args, link, ws, rank, local)
+        run_ours(args, link, coi, ws, rank, local)
     if ws > 1:
         import torch.distributed as dist
         dist.barrier()

@@ -18,7 +18,7 @@ def _run(args, timeout=300):
 
 
 def test_reference_arm_prints_one_contract_line():
-    r = _run(["--impl", "reference", "--config", "c1", "--steps", "1", "--warmup", "1",
+    r = _run(["--impl", "reference", "--config", "c1", "--coi", "0,2", "--steps", "1", "--warmup", "1",
               "--ref-seconds", "0.5"])
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [l for l in r.stdout.splitlines() if l.strip()]
@@ -30,7 +30,8 @@ def test_reference_arm_prints_one_contract_line():
     assert d["impl"] == "reference" and d["value"] > 0 and d["steps"] == 1 and d["warmup"] == 1
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
-    assert d["config"]["workload"].startswith("c1")
+    assert d["config"]["workload"].startswith("c1") and "COIs 0,2" in d["config"]["workload"]
+    assert d["config"]["coi"] == [0, 2] and "COIs [0, 2]" in d["cpu_baseline"]["sample"]
 
 
 def test_product_arm_fails_loudly_without_gpu():
@@ -54,12 +55,24 @@ def test_roofline_unit_counts():
                                                                   2 * 73 + 25 + 2 * 81 + 25)
 
 
-def test_traffic_source_is_the_newest_c2_capture():
+@pytest.mark.parametrize("cfg", ["c2", "c5"])
+def test_traffic_source_is_the_newest_capture_of_the_config(cfg):
     sys.path.insert(0, ROOT)
     import glob
     import bench
-    traffic, src = bench.ncu_traffic()
-    caps = [os.path.basename(f).split("_")[0] for f in glob.glob(os.path.join(ROOT, "profiles", "*ncu_integrand*_c2*.json"))
+    traffic, src = bench.ncu_traffic(cfg)
+    caps = [os.path.basename(f).split("_")[0] for f in glob.glob(os.path.join(ROOT, "profiles", f"*ncu_integrand*_{cfg}*.json"))
             if "fp32" not in f]
     newest = max(caps, key=lambda t: (len(t), t))
     assert src is not None and os.path.basename(src).startswith(newest + "_") and traffic > 0
+
+
+def test_default_workload_is_the_north_star_subset():
+    """The headline is c5 (the 20 THz / 50-span north-star link) on SURVEY 8(d)'s COI subset."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from workloads import bj_config
+    assert bench.parse_coi("default", bj_config("c5")) == [0, 100, 199]
+    assert bench.parse_coi("default", bj_config("c2")) is None
+    assert bench.parse_coi("all", bj_config("c5")) is None
+    assert bench.parse_coi("3,1", bj_config("c5")) == [3, 1]

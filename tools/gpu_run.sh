@@ -22,17 +22,17 @@ if [[ $STAGES == *s* ]]; then
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.log" 2>&1; echo "smoke rc=$?" >> "$OUT/status"
 fi
 if [[ $STAGES == *b* ]]; then
-  timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?" >> "$OUT/status"
+  timeout 900 python bench.py ${BENCH_ARGS:-} > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?" >> "$OUT/status"
 fi
 if [[ $STAGES == *l* ]]; then
-  CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu"
+  CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu ${BENCH_ARGS:-}"
   timeout 300 $CMD > "$OUT/plain_launch.log" 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file "$OUT/launches.csv" $CMD > "$OUT/ncu_launch.log" 2>&1
   echo "launches rc=$?" >> "$OUT/status"
 fi
 if [[ $STAGES == *f* ]]; then
-  CMD="python tools/ncu_target.py --config c2 --reps 2"
+  CMD="python tools/ncu_target.py ${NCU_CFG:---config c5 --coi 100} --reps 2"
   timeout 300 $CMD > "$OUT/plain_full.log" 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:integrand_kernel -s 3 -c 1 \
       -o "$OUT/prof" $CMD > "$OUT/ncu_full.log" 2>&1
