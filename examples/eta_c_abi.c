@@ -59,7 +59,7 @@ int main(void) {
   double eta[NCH];
   if (cudaMemcpy(eta, eta_dev, sizeof(eta), cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
   int64_t pts = 0, ps = 0, nreg = 0;
-  isrs_egn_work(h, &pts, &ps, &nreg);
+  isrs_egn_last_work(h, &pts, &ps, &nreg);
   for (int i = 0; i < NCH; ++i) printf("channel %d  eta %.17e 1/W^2  %.6f dB\n", i, eta[i], 10 * log10(eta[i]));
   printf("regions %lld  points %lld  point-spans %lld\n", (long long)nreg, (long long)pts, (long long)ps);
   cudaFree(eta_dev);

@@ -19,14 +19,28 @@
  * Threading: a handle is not thread-safe; distinct handles are independent.  Successive calls on
  * one handle are ordered on the device even when issued on different streams (a call on a new
  * stream waits for the previous call's end on the device, not on the host).
- * Errors: every call returns a status; on error nothing is enqueued and outputs are untouched;
- * isrs_egn_last_error() (thread-local) names the offending field / index.
- * CUDA graphs: once a handle has run a COI set on a stream, a further isrs_egn_nli for the same COI
- * set on that stream neither allocates nor synchronises the host, so it can be captured with
- * cudaStreamBeginCapture and replayed (the Python Engine.graph() does exactly this).
+ * Devices: every call makes the handle's device current for its duration and restores the
+ * caller's current device before returning.
+ * Asynchrony: isrs_egn_nli / _nli_shard / _combine only enqueue.  A new COI set (or shard) makes
+ * nli rebuild its work list on the host and allocate, upload and free the device copy stream-ordered
+ * on the caller's stream (cudaMallocAsync / cudaMemcpyAsync / cudaFreeAsync), after that stream has
+ * been ordered behind the handle's previous call: no call synchronises the host or the device except
+ * create (synchronous), destroy (synchronises the device) and the inspection calls that say so.
+ * Errors: every call returns a status and isrs_egn_last_error() (thread-local) names the offending
+ * field / index.  Validation, work-list limits, allocation and kernel attributes are checked before
+ * the first kernel is enqueued, so on those errors nothing is enqueued and outputs are untouched; a
+ * CUDA launch failure after that point (ECUDA) may leave a partial enqueue whose outputs are undefined.
+ * CUDA graphs: once a handle has run a COI set (and shard) on a non-capturing stream, a further call
+ * for the same set neither allocates nor synchronises, so it can be captured (cudaStreamBeginCapture)
+ * and replayed; inside a capture the call records no timing or ordering events and leaves
+ * isrs_egn_last_kernel_ms / the cross-stream ordering describing the last direct call (a call that
+ * would have to rebuild its work list inside a capture fails with EINVAL).  A graph bakes in the
+ * handle's work-list buffers: calling that handle with another COI set frees them, so a graph should
+ * own its handle (the Python Engine.graph() creates a private one).
  * Memory: a handle's device buffers come from the device's default stream-ordered memory pool
  * (cudaMallocAsync), whose release threshold the library raises so that repeated create / destroy
  * reuse pool memory; memory a destroyed handle frees stays reserved in that pool for the process.
+ * Tracing: create, nli, nli_shard and eta_host are NVTX ranges of the same names.
  */
 #ifndef ISRS_EGN_H
 #define ISRS_EGN_H
@@ -150,10 +164,17 @@ ISRS_EGN_API int isrs_egn_plan_shards(const isrs_egn_problem *p, const isrs_egn_
 ISRS_EGN_API int isrs_egn_region_partials(isrs_egn_t *h, int32_t n, const int32_t *kappa, const int32_t *k1,
                              const int32_t *k2, double *out_host);
 
-/* Work of the most recent isrs_egn_nli() / isrs_egn_nli_shard() call (synchronises): in-support
- * grid points summed over the regions it launched, point-spans = points * n_span, and the number
- * of regions launched. */
-ISRS_EGN_API int isrs_egn_work(isrs_egn_t *h, int64_t *points, int64_t *point_spans, int64_t *regions);
+/* Work of isrs_egn_nli for a COI set (coi: HOST, NULL = all with n_coi = n_ch), from the host
+ * planner alone (no device access, no synchronisation): exact in-support grid points summed over its
+ * regions (f3 in some closed band, reading C10; a point on a shared edge of touching bands counts
+ * once), point-spans = points * n_span (the work metric, R7), and the number of regions
+ * listed (Eq. 16 generalised). */
+ISRS_EGN_API int isrs_egn_work(const isrs_egn_t *h, int32_t n_coi, const int32_t *coi, int64_t *points,
+                               int64_t *point_spans, int64_t *regions);
+
+/* The same counts for the most recent isrs_egn_nli() / isrs_egn_nli_shard() call, as the kernels
+ * wrote them (synchronises that call): points of the regions it launched (one shard at world > 1). */
+ISRS_EGN_API int isrs_egn_last_work(isrs_egn_t *h, int64_t *points, int64_t *point_spans, int64_t *regions);
 
 /* One-shot end-to-end call with HOST buffers: create + nli (all given COIs) + copy back +
  * destroy.  eta_host [n_coi], terms_host [n_coi * 5] or NULL. */

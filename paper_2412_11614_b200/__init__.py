@@ -35,6 +35,8 @@ class Engine:
 
     def __init__(self, link, grid_n=None, delta_z_m=None, device=0, precision=64,
                  mu_mode=MU_SEGMENT, flags=0, f_samples=0):
+        self._args = (link, dict(grid_n=grid_n, delta_z_m=delta_z_m, device=device, precision=precision,
+                                 mu_mode=mu_mode, flags=flags, f_samples=f_samples))
         self._pa = ProblemArrays(link)
         n = numerics(grid_n if grid_n is not None else link.grid_n,
                      delta_z_m if delta_z_m is not None else getattr(link, "delta_z_m", 1000.0),
@@ -81,9 +83,16 @@ class Engine:
         return out
 
     def work(self):
-        """(points, point_spans, regions) of the last nli call."""
+        """(points, point_spans, regions) of the last nli call, as its kernels counted them."""
         p, ps, r = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
-        _abi.check(_abi.get().isrs_egn_work(self._h, ctypes.byref(p), ctypes.byref(ps), ctypes.byref(r)))
+        _abi.check(_abi.get().isrs_egn_last_work(self._h, ctypes.byref(p), ctypes.byref(ps), ctypes.byref(r)))
+        return p.value, ps.value, r.value
+
+    def planned_work(self, coi=None):
+        """(points, point_spans, regions) of nli(coi) from the host planner alone (no device work)."""
+        n, cp = self._coi(coi)
+        p, ps, r = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _abi.check(_abi.get().isrs_egn_work(self._h, n, cp, ctypes.byref(p), ctypes.byref(ps), ctypes.byref(r)))
         return p.value, ps.value, r.value
 
     def last_kernel_ms(self):
@@ -150,8 +159,10 @@ class Engine:
     def graph(self, coi=None, terms=False):
         """A CUDA graph of one nli call (fixed COI set, fixed output tensors): NliGraph.replay()
         re-runs the whole hot path (fork, both integrand launches, join, reduce) as one graph
-        launch -- for small links whose call is launch-bound (c1: 45 -> 31 us per call)."""
-        return NliGraph(self, coi, terms)
+        launch -- for small links whose call is launch-bound (c1: 45 -> 31 us per call).  The graph
+        owns a private handle on the same link, so this Engine stays free for other COI sets."""
+        link, kw = self._args
+        return NliGraph(Engine(link, **kw), coi, terms, own=True)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -175,10 +186,11 @@ class NliGraph:
     """Captured isrs_egn_nli (torch.cuda.CUDAGraph).  The work list of the COI set is built and the
     handle is warmed up on the graph's own stream before capture (no host synchronisation or
     allocation happens inside it).  replay() writes the captured output tensors `eta` (and `terms`),
-    ordered after the caller's current stream, which waits for it.  The graph keeps the handle's device buffers: do not call the handle
-    with another COI set while replaying."""
+    ordered after the caller's current stream, which waits for it.  The graph bakes in its handle's
+    device buffers, so it owns that handle (Engine.graph() passes a private one, own=True) and
+    closes it with close()."""
 
-    def __init__(self, engine, coi=None, terms=False):
+    def __init__(self, engine, coi=None, terms=False, own=False):
         import torch
         dev = torch.device("cuda", engine.device)
         n = engine.n_ch if coi is None else len(coi)
@@ -186,6 +198,7 @@ class NliGraph:
         self.terms = torch.empty((n, 5), dtype=torch.float64, device=dev) if terms else None
         self.stream = torch.cuda.Stream(device=dev)
         self._engine = engine
+        self._own = own
         tp = self.terms.data_ptr() if terms else 0
         with torch.cuda.stream(self.stream):
             for _ in range(2):
@@ -204,6 +217,21 @@ class NliGraph:
             self.graph.replay()
         cur.wait_stream(self.stream)
         return (self.eta, self.terms) if self.terms is not None else self.eta
+
+    def close(self):
+        if getattr(self, "graph", None) is not None:
+            self.stream.synchronize()
+            self.graph.reset()
+            self.graph = None
+        if self._own and self._engine is not None:
+            self._engine.close()
+            self._engine = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def plan_shards(link, world, coi=None, grid_n=None, delta_z_m=None, f_samples=0):

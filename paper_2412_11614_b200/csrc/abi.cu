@@ -20,6 +20,8 @@
 #include <tuple>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/isrs_egn.h"
 #include "internal.h"
 
@@ -35,85 +37,78 @@ int fail(int code, const std::string& msg) {
 }
 
 // Device allocations come from the device's default stream-ordered memory pool with the release
-// threshold raised, so repeated create / destroy (the one-shot isrs_egn_eta_host path) reuse pool
-// memory instead of mapping and unmapping it through the driver each time.  Allocation is on the
-// legacy default stream and completed before the buffer is handed out; frees follow a device
-// synchronisation (the buffer may be in use on any stream), as cudaFree would.
-static cudaError_t dev_alloc(void** p, size_t bytes) {
+// threshold raised, so repeated create / destroy (the one-shot isrs_egn_eta_host path) and work-list
+// rebuilds reuse pool memory instead of mapping and unmapping it through the driver each time.
+// Every allocation and free is stream-ordered (cudaMallocAsync / cudaFreeAsync on a given stream):
+// create() uses the legacy default stream and then synchronises it (create is synchronous by
+// contract); a work-list rebuild inside isrs_egn_nli allocates, uploads and frees on the caller's
+// stream after that stream has been ordered behind the handle's previous call, so nli never
+// synchronises the host or the device.
+static void tune_pool(int dev) {
+  static std::mutex mu;
+  static std::set<int> tuned;
+  std::lock_guard<std::mutex> lk(mu);
+  if (tuned.count(dev)) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  tuned.insert(dev);
+}
+
+static cudaError_t dev_alloc_on(void** p, size_t bytes, cudaStream_t st) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  {
-    static std::mutex mu;
-    static std::set<int> tuned;
-    std::lock_guard<std::mutex> lk(mu);
-    if (!tuned.count(dev)) {
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-      }
-      tuned.insert(dev);
-    }
-  }
-  e = cudaMallocAsync(p, bytes, 0);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(0);
-  return e;
+  tune_pool(dev);
+  return cudaMallocAsync(p, bytes, st);
 }
 
-static void dev_free(void* p) {
-  if (!p) return;
-  cudaDeviceSynchronize();
-  cudaFreeAsync(p, 0);
+// Stream-ordered free: `st` must already be ordered after every use of p.
+static void dev_free_on(void* p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
 }
+
+// RAII: make `dev` current for the duration of an API call and restore the caller's device after
+// (a process may hold handles on several GPUs; torch's current device must not move).
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// NVTX ranges around the public entry points (visible in nsys / ncu --nvtx)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
-  bool owned = true;   // false: p points into an Arena (one allocation for many buffers)
-  ~DevBuf() { reset(); }
-  void reset() {
-    if (p && owned) dev_free(p);
-    p = nullptr;
-    n = 0;
-    owned = true;
-  }
-  void borrow(T* q, size_t cnt) {
-    reset();
+  void borrow(T* q, size_t cnt) {   // buffers live inside an Arena (one allocation for many)
     p = q;
     n = cnt;
-    owned = false;
   }
-  bool alloc(size_t count) {
-    reset();
-    if (count == 0) count = 1;
-    void* q = nullptr;
-    if (dev_alloc(&q, count * sizeof(T)) != cudaSuccess) {
-      p = nullptr;
-      return false;
-    }
-    p = static_cast<T*>(q);
-    n = count;
-    return true;
-  }
-  bool upload(const std::vector<T>& v) {
-    if (!alloc(v.size())) return false;
-    if (v.empty()) return true;
-    return cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice) == cudaSuccess;
+  void clear() {
+    p = nullptr;
+    n = 0;
   }
 };
 
-// One device allocation holding many small buffers (fewer cudaMalloc / cudaFree calls on the
-// create / plan path): buffers with host data are staged into one host block and copied with ONE
-// cudaMemcpy; device-only buffers follow them uninitialised.
+// One device allocation holding many small buffers (fewer allocations on the create / plan path).
 struct Arena {
   char* base = nullptr;
-  ~Arena() { reset(); }
-  void reset() {
-    if (base) dev_free(base);
-    base = nullptr;
-  }
+  cudaStream_t st = nullptr;   // stream the allocation was made on (its free follows in that order)
 };
 
 class Packer {
@@ -137,26 +132,34 @@ class Packer {
     dev_.push_back({[d, cnt](char* q) { d->borrow(reinterpret_cast<T*>(q), cnt); }, nullptr,
                     cnt * sizeof(T), 0});
   }
-  bool commit(Arena* a) {
+  // Allocate one block on `st` and upload the staged host data (stream-ordered; a pageable-source
+  // cudaMemcpyAsync returns once the data is staged, so the host vectors may die on return).  Only
+  // when both succeed is the old arena freed (on `st`, which the caller has ordered after its last
+  // use) and are the DevBufs rebound: on failure the handle keeps its previous, valid buffers.
+  cudaError_t commit(Arena* a, cudaStream_t st) {
     size_t off = 0;
     for (auto& e : init_) { e.off = off; off += up(e.bytes); }
     const size_t init_bytes = off;
     for (auto& e : dev_) { e.off = off; off += up(e.bytes); }
-    a->reset();
     void* q = nullptr;
-    if (dev_alloc(&q, std::max<size_t>(off, 256)) != cudaSuccess) {
-      a->base = nullptr;
-      return false;
+    cudaError_t ce = dev_alloc_on(&q, std::max<size_t>(off, 256), st);
+    if (ce != cudaSuccess) return ce;
+    if (init_bytes) {
+      std::vector<char> stage(init_bytes);
+      for (auto& e : init_)
+        if (e.bytes) std::memcpy(stage.data() + e.off, e.src, e.bytes);
+      ce = cudaMemcpyAsync(q, stage.data(), init_bytes, cudaMemcpyHostToDevice, st);
+      if (ce != cudaSuccess) {
+        dev_free_on(q, st);
+        return ce;
+      }
     }
+    if (a->base) dev_free_on(a->base, st);
     a->base = static_cast<char*>(q);
-    std::vector<char> stage(init_bytes);
-    for (auto& e : init_) {
-      if (e.bytes) std::memcpy(stage.data() + e.off, e.src, e.bytes);
-      e.bind(a->base + e.off);
-    }
+    a->st = st;
+    for (auto& e : init_) e.bind(a->base + e.off);
     for (auto& e : dev_) e.bind(a->base + e.off);
-    return init_bytes == 0 ||
-           cudaMemcpy(a->base, stage.data(), init_bytes, cudaMemcpyHostToDevice) == cudaSuccess;
+    return cudaSuccess;
   }
 };
 
@@ -179,7 +182,7 @@ struct isrs_egn {
   std::vector<double> lo, hi, f, G, R, P, phi, psi, delta;
   std::vector<long long> rate;
   double f_c = 0, b_tot = 0, p_tot = 0;
-  // device data
+  // device data (views into the arenas)
   DevBuf<double> d_lo, d_hi, d_f, d_G, d_R, d_P, d_phi, d_psi, d_delta;
   DevBuf<long long> d_rate;
   DevBuf<double> d_A2, d_A3, d_Eh, d_ah, d_gh, d_macc, d_aL;
@@ -193,18 +196,19 @@ struct isrs_egn {
   int kstride = 0, tstride = 0, tw = 0;
   // work list cache (last call)
   WorkList wl;
-  bool wl_all = false;
+  bool have_wl = false;
   DevBuf<RegionDesc> d_desc;
   DevBuf<long long> d_coi_off;
   DevBuf<int> d_coi, d_list_d, d_list_c;
   DevBuf<double> d_fv;
   // regions launched by the last call (the whole list, or one shard of it)
   std::vector<int> act_d, act_c;
+  std::vector<int> sh_act_d, sh_act_c;   // the regions of the current shard (rank, world)
   int sh_rank = -1, sh_world = -1;
   long long sh_lo = 0, sh_hi = 0;
   DevBuf<int> d_sh_d, d_sh_c;
   DevBuf<double> d_partials, d_npts;
-  Arena arena_create, arena_plan;   // declared after the DevBufs: destroyed first
+  Arena arena_create, arena_plan, arena_shard;
   cudaStream_t last_stream = nullptr;
   bool have_result = false;
   int last_launches = 0;
@@ -212,14 +216,19 @@ struct isrs_egn {
   // coherent-region integrand on a side stream, concurrent with the D-only launch (fills its tail)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, evc[2] = {nullptr, nullptr};
+  // fork / join events used only while the caller's stream is being captured into a CUDA graph
+  // (the timing and ordering events above are never recorded inside a capture)
+  cudaEvent_t cap_fork = nullptr, cap_join = nullptr;
   bool launched[2] = {false, false};
-  ~isrs_egn() {
+  ~isrs_egn() {   // isrs_egn_destroy synchronises the device first
+    for (Arena* a : {&arena_plan, &arena_shard, &arena_create})
+      if (a->base) cudaFreeAsync(a->base, 0);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : evc)
       if (e) cudaEventDestroy(e);
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_join) cudaEventDestroy(ev_join);
+    for (cudaEvent_t e : {ev_fork, ev_join, cap_fork, cap_join})
+      if (e) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
   }
 };
@@ -372,9 +381,11 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
   *out = nullptr;
   isrs_egn_numerics num = n ? *n : isrs_egn_numerics{};
   if (num.precision == 0) num.precision = 64;
+  NvtxRange nv("isrs_egn_create");
   int rc = validate(p, &num);
   if (rc) return rc;
-  cudaError_t ce = cudaSetDevice(device);
+  DeviceGuard dg(device);
+  cudaError_t ce = dg.err;
   if (ce != cudaSuccess) return cuda_fail(ce, "cudaSetDevice");
 
   auto* h = new isrs_egn();
@@ -503,29 +514,67 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
   pk.add(&h->d_gamma, vG); pk.add(&h->d_pcr, vP); pk.add(&dL, cL); pk.add(&dA, cA); pk.add(&dC, cC);
   pk.reserve(&h->d_lnA, (size_t)h->n_cls * h->kstride);
   pk.reserve(&h->d_zeta, (size_t)h->n_cls * h->kstride);
-  const bool ok = pk.commit(&h->arena_create);
-  if (!ok) {
+  // create is synchronous: upload and precompute on the legacy default stream, then wait for it
+  ce = pk.commit(&h->arena_create, nullptr);
+  if (ce != cudaSuccess) {
+    cudaStreamSynchronize(nullptr);
     delete h;
-    return fail(ISRS_EGN_ENOMEM, "device allocation/upload failed");
+    return fail(ISRS_EGN_ENOMEM, std::string("device allocation/upload failed: ") + cudaGetErrorString(ce));
   }
   PParams pp{dL.p, dA.p, dC.p, h->d_Kc.p, h->n_cls, h->kstride, h->p_tot, h->b_tot, h->d_lnA.p, h->d_zeta.p};
-  if (launch_precompute(pp, nullptr) != 0) {
+  const int lrc = launch_precompute(pp, nullptr);
+  ce = cudaStreamSynchronize(nullptr);
+  if (lrc != 0 || ce != cudaSuccess) {
     delete h;
-    return cuda_fail(cudaGetLastError(), "precompute launch");
-  }
-  ce = cudaDeviceSynchronize();
-  if (ce != cudaSuccess) {
-    delete h;
-    return cuda_fail(ce, "precompute");
+    return cuda_fail(lrc != 0 ? cudaGetLastError() : ce, "precompute");
   }
   *out = h;
   return ISRS_EGN_OK;
 }
 
-// Number of in-support grid points of region (f, k1, k2), counted per lattice line j = a m1 + b m2
-// (f3 constant on a line) -- the integrand kernel's cost of the region.  Used only to order the
-// launch list (largest regions first, so the last wave of CTAs is short); ties at touching band
-// edges may be counted twice, which does not matter for ordering.
+// sum_{i=0}^{n-1} floor((a i + b) / m) for n, m >= 1, a, b >= 0 (Euclid-like reduction, O(log)).
+static long long floor_sum(long long n, long long m, long long a, long long b) {
+  long long ans = 0;
+  while (true) {
+    if (a >= m) { ans += (n - 1) * n / 2 * (a / m); a %= m; }
+    if (b >= m) { ans += n * (b / m); b %= m; }
+    const long long y_max = a * n + b;
+    if (y_max < m) break;
+    n = y_max / m;
+    b = y_max % m;
+    std::swap(m, a);
+  }
+  return ans;
+}
+
+// Grid points of a region on lattice lines j' <= j, i.e. #{(m1, m2) in [0, N)^2 : a m1 + b m2 <= j}
+// = sum over m1 <= j/a of min(N, floor((j - a m1)/b) + 1): the m1 with j - a m1 >= b (N - 1) give N
+// each, the others a floor sum.
+static long long lattice_cum(int N, int a, int b, long long j) {
+  if (j < 0) return 0;
+  const long long m_hi = std::min<long long>(N - 1, j / a);           // last m1 with j - a m1 >= 0
+  const long long full = j - (long long)b * (N - 1);                  // j - a m1 >= b (N-1) <=> m1 <= full / a
+  const long long m_full = full < 0 ? -1 : std::min(m_hi, full / a);  // m1 in [0, m_full]: N points
+  long long tot = (m_full + 1) * N;
+  const long long cnt = m_hi - m_full;                               // m1 in (m_full, m_hi]
+  if (cnt > 0) {
+    // i = m_hi - m1 in [0, cnt): floor((j - a m_hi + a i) / b) + 1
+    tot += floor_sum(cnt, b, a, j - (long long)a * m_hi) + cnt;
+  }
+  return tot;
+}
+
+static long long floor_div(long long x, long long y) { return x / y - ((x % y != 0) && ((x < 0) != (y < 0))); }
+static long long ceil_div(long long x, long long y) { return -floor_div(-x, y); }
+
+// Exact number of in-support grid points of region (f, k1, k2) -- the integrand kernel's cost of the
+// region and the work metric.  On a lattice line j = a m1 + b m2 (a:b = R1:R2 in lowest terms) f3 =
+// C + g j is constant; the lines whose f3 lies in some closed band [lo_c, hi_c] (reading C10: an edge
+// tie is in support, counted once even when two bands touch there) form a union of j-intervals, one
+// per band, merged where touching bands share an edge line; the points on lines j0..j1 are
+// lattice_cum(j1) - lattice_cum(j0 - 1).  All frequencies are multiples of 1/4 Hz (integer-Hz inputs,
+// f_c the midpoint of half-integer edges), so the interval ends are computed in exact integers.
+// O(bands x (1 or N)) per region instead of a walk over every point.
 static long long region_points(const isrs_egn* h, double f, int k1, int k2) {
   const int N = h->N, nc = h->n_ch;
   const long long r1 = h->rate[k1], r2 = h->rate[k2];
@@ -535,35 +584,25 @@ static long long region_points(const isrs_egn* h, double f, int k1, int k2) {
   const double d1 = h->delta[k1], d2 = h->delta[k2];
   const double g = d1 / a;
   const double C = h->lo[k1] + h->lo[k2] - f + (0.5 * d1 + 0.5 * d2);
-  const int J = (a + b) * (N - 1) + 1;
-  long long cnt = 0;
-  if (a == 1 && b == 1) {
-    auto P = [&](long long j) -> long long {   // sum_{i<=j} min(i, 2N-2-i) + 1
-      if (j < 0) return 0;
-      if (j < N) return (j + 1) * (j + 2) / 2;
-      return (long long)N * N - (2LL * N - 2 - j) * (2LL * N - 1 - j) / 2;
-    };
-    const double f3max = C + g * (J - 1);
-    for (int c = (int)(std::lower_bound(h->hi.begin(), h->hi.end(), C) - h->hi.begin());
-         c < nc && h->lo[c] <= f3max; ++c) {
-      const long long j0 = std::max(0LL, (long long)std::ceil((h->lo[c] - C) / g));
-      const long long j1 = std::min((long long)J - 1, (long long)std::floor((h->hi[c] - C) / g));
-      if (j0 <= j1) cnt += P(j1) - P(j0 - 1);
+  const long long J = (long long)(a + b) * (N - 1) + 1;
+  auto q4 = [](double v) { return (long long)std::llround(4.0 * v); };
+  const long long C4 = q4(C), g4 = q4(g);
+  const double f3max = C + g * (double)(J - 1);
+  long long cnt = 0, cur0 = 0, cur1 = -2;     // current merged interval [cur0, cur1]
+  for (int c = (int)(std::lower_bound(h->hi.begin(), h->hi.end(), C) - h->hi.begin());
+       c < nc && h->lo[c] <= f3max; ++c) {
+    const long long j0 = std::max(0LL, ceil_div(q4(h->lo[c]) - C4, g4));
+    const long long j1 = std::min(J - 1, floor_div(q4(h->hi[c]) - C4, g4));
+    if (j0 > j1) continue;
+    if (j0 <= cur1) {                         // touching bands share the edge line
+      cur1 = std::max(cur1, j1);
+      continue;
     }
-    return cnt;
+    if (cur1 >= cur0) cnt += lattice_cum(N, a, b, cur1) - lattice_cum(N, a, b, cur0 - 1);
+    cur0 = j0;
+    cur1 = j1;
   }
-  int c = (int)(std::lower_bound(h->hi.begin(), h->hi.end(), C) - h->hi.begin());
-  for (int j = 0; j < J; ++j) {
-    const double f3 = C + g * j;
-    while (c < nc && h->hi[c] < f3) ++c;
-    if (c >= nc) break;
-    if (h->lo[c] > f3) continue;
-    int lowb = j - b * (N - 1);
-    lowb = (lowb <= 0) ? 0 : (lowb + a - 1) / a;
-    const int upb = std::min(N - 1, j / a);
-    for (int m1 = lowb; m1 <= upb; ++m1)
-      if ((j - a * m1) % b == 0) ++cnt;
-  }
+  if (cur1 >= cur0) cnt += lattice_cum(N, a, b, cur1) - lattice_cum(N, a, b, cur0 - 1);
   return cnt;
 }
 
@@ -600,9 +639,6 @@ static void build_worklist(const isrs_egn* h, const std::vector<int>& coi, WorkL
         if (h->phi[k2] != 0.0 && overlaps(k2)) flags |= NEED_F;
         if (h->phi[k1] != 0.0 && k1 == k2) flags |= NEED_G;
         if (h->psi[k1] != 0.0 && k1 == k2 && overlaps(k1)) flags |= NEED_H;
-        if (h->num.flags & ISRS_EGN_FLAG_UNIT_LINK) {
-          // unit link hook: same gating
-        }
         const int id = (int)w->desc.size();
         w->desc.push_back(RegionDesc{kappa, k1, k2, flags | (fvi << FV_SHIFT)});
         (flags ? w->list_c : w->list_d).push_back(id);
@@ -655,46 +691,106 @@ static void shard_range(const WorkList& w, int rank, int world, long long* lo, l
 
 // The hot path: integrand over the regions of shard (rank, world) of the COI set, then either the
 // per-COI assembly into eta (part_out == NULL; world must be 1) or the raw per-COI sums.
+// Asynchronous on `st`: a new COI set (or shard) rebuilds the work list on the host and allocates,
+// uploads and frees its device copy stream-ordered on `st` -- no host or device synchronisation.
+// Every check that can fail (work-list limits, allocation, kernel attributes, pending errors) runs
+// before the first kernel is enqueued; a failure after that point is a CUDA launch error (ECUDA).
+// While `st` is being captured into a CUDA graph the call only enqueues kernels (no allocation: the
+// work list must exist already, no timing or ordering events; fork / join use capture-only events).
 static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, double* eta_dev,
                    double* terms_dev, double* part_out, cudaStream_t st) {
-  cudaError_t ce = cudaSetDevice(h->device);
-  if (ce != cudaSuccess) return cuda_fail(ce, "cudaSetDevice");
-  ce = cudaGetLastError();
+  DeviceGuard dg(h->device);
+  if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+  cudaError_t ce = cudaGetLastError();
   if (ce != cudaSuccess) return cuda_fail(ce, "pending CUDA error");
-  if (!(h->have_result || h->wl.desc.size()) || h->wl.coi != c) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  ce = cudaStreamIsCapturing(st, &cap);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamIsCapturing");
+  const bool capturing = cap != cudaStreamCaptureStatusNone;
+  const bool rebuild = !h->have_wl || h->wl.coi != c;
+  const bool reshard = world > 1 && (rebuild || h->sh_rank != rank || h->sh_world != world);
+  if (capturing && (rebuild || reshard))
+    return fail(ISRS_EGN_EINVAL, "stream capture: call isrs_egn_nli once with this COI set (and shard) "
+                                 "on a non-capturing stream first, so that nothing is allocated inside the capture");
+  if (rebuild) {
     // region ids are int32 and the f-sample index lives in 23 flag bits
     const double nreg_max = (double)c.size() * std::max(1, h->num.f_samples) * h->n_ch * h->n_ch;
     if (nreg_max > 2147483647.0 || (double)c.size() * std::max(1, h->num.f_samples) >= 8388608.0)
       return fail(ISRS_EGN_ERANGE, "n_coi x f_samples x n_ch^2 regions exceed the 2^31 work-list limit");
-    // (re)build and upload the work list for this COI set (cached across identical calls)
-    cudaStreamSynchronize(h->last_stream);
-    build_worklist(h, c, &h->wl);
+  }
+  if (!h->ev[0]) {
+    for (auto& e : h->ev)
+      if (cudaEventCreate(&e) != cudaSuccess) return cuda_fail(cudaGetLastError(), "cudaEventCreate");
+  }
+  if (!h->side) {
+    if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->cap_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->cap_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreate(&h->evc[0]) != cudaSuccess || cudaEventCreate(&h->evc[1]) != cudaSuccess)
+      return cuda_fail(cudaGetLastError(), "side stream / events");
+  }
+  const int mode = (h->num.flags & ISRS_EGN_FLAG_UNIT_LINK) ? MODE_UNIT
+                   : (h->num.mu_mode == ISRS_EGN_MU_INTEGRAL ? MODE_QUAD
+                   : (h->num.mu_mode == ISRS_EGN_MU_MACLAURIN ? MODE_MACLAURIN
+                      : (h->num.precision == 32 ? MODE_SEG32
+                         : ((h->num.flags & ISRS_EGN_FLAG_DEDUP) ? MODE_SEGDD
+                            : ((h->num.flags & ISRS_EGN_FLAG_LITERAL_GAIN) ? MODE_SEGLG : MODE_SEGMENT)))));
+  if (integrand_prepare(mode, h->tstride, h->tw, h->N) != 0)
+    return cuda_fail(cudaGetLastError(), "integrand kernel attributes");
+  // calls on one handle share its partials (and a rebuild frees the previous work list): a call on
+  // another stream than the previous one waits (on the device) for the previous call's end
+  if (!capturing && h->have_result && st != h->last_stream) cudaStreamWaitEvent(st, h->ev[3], 0);
+  if (rebuild) {
+    WorkList wl;
+    build_worklist(h, c, &wl);
     Packer pk;
-    pk.add(&h->d_desc, h->wl.desc); pk.add(&h->d_coi_off, h->wl.coi_off); pk.add(&h->d_coi, h->wl.coi);
-    pk.add(&h->d_list_d, h->wl.list_d); pk.add(&h->d_list_c, h->wl.list_c); pk.add(&h->d_fv, h->wl.fv);
-    pk.reserve(&h->d_partials, h->wl.desc.size() * 6);
-    pk.reserve(&h->d_npts, c.size());
-    if (!pk.commit(&h->arena_plan)) return fail(ISRS_EGN_ENOMEM, "work-list allocation failed");
+    DevBuf<RegionDesc> desc;
+    DevBuf<long long> coi_off;
+    DevBuf<int> coi_d, list_d, list_c;
+    DevBuf<double> fv, partials, npts;
+    pk.add(&desc, wl.desc); pk.add(&coi_off, wl.coi_off); pk.add(&coi_d, wl.coi);
+    pk.add(&list_d, wl.list_d); pk.add(&list_c, wl.list_c); pk.add(&fv, wl.fv);
+    pk.reserve(&partials, wl.desc.size() * 6);
+    pk.reserve(&npts, c.size());
+    ce = pk.commit(&h->arena_plan, st);      // on failure the handle keeps its previous work list
+    if (ce != cudaSuccess) return fail(ISRS_EGN_ENOMEM, std::string("work-list allocation failed: ") + cudaGetErrorString(ce));
+    h->d_desc = desc; h->d_coi_off = coi_off; h->d_coi = coi_d; h->d_list_d = list_d;
+    h->d_list_c = list_c; h->d_fv = fv; h->d_partials = partials; h->d_npts = npts;
+    h->wl = std::move(wl);
+    h->have_wl = true;
     h->sh_rank = h->sh_world = -1;
   }
   const int* dl_d = h->d_list_d.p;
   const int* dl_c = h->d_list_c.p;
   long long r_lo = 0, r_hi = (long long)h->wl.desc.size();
+  std::vector<int> act_d, act_c;
   if (world > 1) {
-    if (h->sh_rank != rank || h->sh_world != world) {
-      cudaStreamSynchronize(h->last_stream);
-      shard_range(h->wl, rank, world, &h->sh_lo, &h->sh_hi);
-      h->act_d.clear();
-      h->act_c.clear();
+    if (reshard) {
+      long long lo, hi;
+      shard_range(h->wl, rank, world, &lo, &hi);
       for (int id : h->wl.list_d)
-        if (id >= h->sh_lo && id < h->sh_hi) h->act_d.push_back(id);
+        if (id >= lo && id < hi) act_d.push_back(id);
       for (int id : h->wl.list_c)
-        if (id >= h->sh_lo && id < h->sh_hi) h->act_c.push_back(id);
-      if (!h->d_sh_d.upload(h->act_d) || !h->d_sh_c.upload(h->act_c))
-        return fail(ISRS_EGN_ENOMEM, "shard list allocation failed");
+        if (id >= lo && id < hi) act_c.push_back(id);
+      Packer pk;
+      DevBuf<int> sd, sc;
+      pk.add(&sd, act_d);
+      pk.add(&sc, act_c);
+      ce = pk.commit(&h->arena_shard, st);
+      if (ce != cudaSuccess) return fail(ISRS_EGN_ENOMEM, std::string("shard list allocation failed: ") + cudaGetErrorString(ce));
+      h->d_sh_d = sd;
+      h->d_sh_c = sc;
+      h->sh_lo = lo;
+      h->sh_hi = hi;
       h->sh_rank = rank;
       h->sh_world = world;
+      h->sh_act_d = std::move(act_d);
+      h->sh_act_c = std::move(act_c);
     }
+    h->act_d = h->sh_act_d;
+    h->act_c = h->sh_act_c;
     dl_d = h->d_sh_d.p;
     dl_c = h->d_sh_c.p;
     r_lo = h->sh_lo;
@@ -719,16 +815,7 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
   kp.lnA = h->d_lnA.p; kp.zeta = h->d_zeta.p; kp.Kc = h->d_Kc.p; kp.n_cls = h->n_cls;
   kp.kstride = h->kstride; kp.tstride = h->tstride; kp.tw = h->tw; kp.N = h->N;
   kp.fv = h->d_fv.p; kp.desc = h->d_desc.p; kp.partials = h->d_partials.p;
-  kp.mode = (h->num.flags & ISRS_EGN_FLAG_UNIT_LINK) ? MODE_UNIT
-            : (h->num.mu_mode == ISRS_EGN_MU_INTEGRAL ? MODE_QUAD
-            : (h->num.mu_mode == ISRS_EGN_MU_MACLAURIN ? MODE_MACLAURIN
-               : (h->num.precision == 32 ? MODE_SEG32
-                  : ((h->num.flags & ISRS_EGN_FLAG_DEDUP) ? MODE_SEGDD
-                     : ((h->num.flags & ISRS_EGN_FLAG_LITERAL_GAIN) ? MODE_SEGLG : MODE_SEGMENT)))));
-  if (!h->ev[0]) {
-    for (auto& e : h->ev)
-      if (cudaEventCreate(&e) != cudaSuccess) return cuda_fail(cudaGetLastError(), "cudaEventCreate");
-  }
+  kp.mode = mode;
   int launches = 0;
 #ifdef ISRS_PROF
   static unsigned long long* d_prof = nullptr;
@@ -736,39 +823,32 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
   cudaMemsetAsync(d_prof, 0, 16 * sizeof(unsigned long long), st);
   kp.prof = d_prof;
 #endif
-  if (!h->side) {
-    if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreate(&h->evc[0]) != cudaSuccess || cudaEventCreate(&h->evc[1]) != cudaSuccess)
-      return cuda_fail(cudaGetLastError(), "side stream / events");
-  }
-  // calls on one handle share its partials: a call on another stream than the previous one waits
-  // (on the device) for the previous call's end, so successive calls stay ordered
-  if (h->have_result && st != h->last_stream) cudaStreamWaitEvent(st, h->ev[3], 0);
   // fork: the coherent regions run on the side stream while the D-only regions run on `st`;
   // join before the per-COI reduce.  ev[0] -> ev[2] brackets the whole integrand phase.
-  cudaEventRecord(h->ev[0], st);
-  cudaEventRecord(h->ev_fork, st);
-  cudaStreamWaitEvent(h->side, h->ev_fork, 0);
-  cudaEventRecord(h->evc[0], h->side);
+  cudaEvent_t fork = capturing ? h->cap_fork : h->ev_fork, join = capturing ? h->cap_join : h->ev_join;
+  if (!capturing) cudaEventRecord(h->ev[0], st);
+  cudaEventRecord(fork, st);
+  cudaStreamWaitEvent(h->side, fork, 0);
+  if (!capturing) cudaEventRecord(h->evc[0], h->side);
   if (launch_integrand(kp, dl_c, (long long)h->act_c.size(), true, h->side, &launches) != 0)
     return cuda_fail(cudaGetLastError(), "integrand launch (coherent regions)");
-  cudaEventRecord(h->evc[1], h->side);
-  cudaEventRecord(h->ev_join, h->side);
+  if (!capturing) cudaEventRecord(h->evc[1], h->side);
+  cudaEventRecord(join, h->side);
   if (launch_integrand(kp, dl_d, (long long)h->act_d.size(), false, st, &launches) != 0)
     return cuda_fail(cudaGetLastError(), "integrand launch (D-only regions)");
-  cudaEventRecord(h->ev[1], st);
-  cudaStreamWaitEvent(st, h->ev_join, 0);
-  cudaEventRecord(h->ev[2], st);
-  h->launched[0] = !h->act_d.empty();
-  h->launched[1] = !h->act_c.empty();
+  if (!capturing) cudaEventRecord(h->ev[1], st);
+  cudaStreamWaitEvent(st, join, 0);
+  if (!capturing) cudaEventRecord(h->ev[2], st);
   RParams rp{h->d_desc.p, h->d_partials.p, h->d_coi_off.p, h->d_coi.p, h->d_G.p, h->d_R.p,
              h->d_P.p, h->d_phi.p, h->d_psi.p, (int)c.size(),
              1.0 / std::max(1, h->num.f_samples), eta_dev, terms_dev, h->d_npts.p, r_lo, r_hi,
              part_out};
   if (launch_reduce(rp, st) != 0) return cuda_fail(cudaGetLastError(), "reduce launch");
+  launches += 1;
+  if (capturing) return ISRS_EGN_OK;     // the handle's timing / ordering state describes direct calls
   cudaEventRecord(h->ev[3], st);
+  h->launched[0] = !h->act_d.empty();
+  h->launched[1] = !h->act_c.empty();
 #ifdef ISRS_PROF
   {
     unsigned long long hp[16];
@@ -786,7 +866,6 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
             hp[10] ? (double)hp[12] / hp[10] : 0.0);
   }
 #endif
-  launches += 1;
   h->last_launches = launches;
   h->last_stream = st;
   h->have_result = true;
@@ -797,6 +876,7 @@ extern "C" int isrs_egn_nli(isrs_egn_t* h, int32_t n_coi, const int32_t* coi, do
                             double* terms_dev, void* cuda_stream) {
   if (!h) return fail(ISRS_EGN_EINVAL, "handle is NULL");
   if (!eta_dev) return fail(ISRS_EGN_EINVAL, "eta_dev is NULL");
+  NvtxRange nv("isrs_egn_nli");
   std::vector<int> c;
   int rc = coi_list(h, n_coi, coi, &c);
   if (rc) return rc;
@@ -807,6 +887,7 @@ extern "C" int isrs_egn_nli_shard(isrs_egn_t* h, int32_t n_coi, const int32_t* c
                                   int32_t world, double* coi_sums_dev, void* cuda_stream) {
   if (!h) return fail(ISRS_EGN_EINVAL, "handle is NULL");
   if (!coi_sums_dev) return fail(ISRS_EGN_EINVAL, "coi_sums_dev is NULL");
+  NvtxRange nv("isrs_egn_nli_shard");
   if (world < 1 || rank < 0 || rank >= world) return fail(ISRS_EGN_EINVAL, "rank/world out of range");
   std::vector<int> c;
   int rc = coi_list(h, n_coi, coi, &c);
@@ -823,9 +904,10 @@ extern "C" int isrs_egn_combine(isrs_egn_t* h, int32_t n_coi, const int32_t* coi
   std::vector<int> c;
   int rc = coi_list(h, n_coi, coi, &c);
   if (rc) return rc;
-  cudaError_t ce = cudaSetDevice(h->device);
-  if (ce != cudaSuccess) return cuda_fail(ce, "cudaSetDevice");
-  if (h->wl.coi != c || !h->d_coi.p) return fail(ISRS_EGN_EINVAL, "combine: COI set differs from the last shard call");
+  DeviceGuard dg(h->device);
+  if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+  if (!h->have_wl || h->wl.coi != c || !h->d_coi.p)
+    return fail(ISRS_EGN_EINVAL, "combine: COI set differs from the last shard call");
   CParams cp{gathered_dev, world, h->d_coi.p, h->d_R.p, h->d_P.p, (int)c.size(),
              1.0 / std::max(1, h->num.f_samples), eta_dev, terms_dev, nullptr};
   if (launch_combine(cp, cuda_stream) != 0) return cuda_fail(cudaGetLastError(), "combine launch");
@@ -864,8 +946,9 @@ extern "C" int isrs_egn_region_partials(isrs_egn_t* h, int32_t n, const int32_t*
   if (!h || !out_host || n < 0 || (n > 0 && (!kappa || !k1 || !k2)))
     return fail(ISRS_EGN_EINVAL, "bad argument");
   if (!h->have_result) return fail(ISRS_EGN_EINVAL, "no isrs_egn_nli() result yet");
-  cudaError_t ce = cudaStreamSynchronize(h->last_stream);
-  if (ce != cudaSuccess) return cuda_fail(ce, "stream sync");
+  DeviceGuard dg(h->device);
+  cudaError_t ce = cudaEventSynchronize(h->ev[3]);
+  if (ce != cudaSuccess) return cuda_fail(ce, "event sync");
   const auto& w = h->wl;
   for (int q = 0; q < n; ++q) {
     double* o = out_host + 6 * (size_t)q;
@@ -885,11 +968,28 @@ extern "C" int isrs_egn_region_partials(isrs_egn_t* h, int32_t n, const int32_t*
   return ISRS_EGN_OK;
 }
 
-extern "C" int isrs_egn_work(isrs_egn_t* h, int64_t* points, int64_t* point_spans, int64_t* regions) {
+extern "C" int isrs_egn_work(const isrs_egn_t* h, int32_t n_coi, const int32_t* coi, int64_t* points,
+                             int64_t* point_spans, int64_t* regions) {
+  if (!h) return fail(ISRS_EGN_EINVAL, "handle is NULL");
+  std::vector<int> c;
+  int rc = coi_list(h, n_coi, coi, &c);
+  if (rc) return rc;
+  WorkList w;
+  build_worklist(h, c, &w);   // host planner only: exact in-support point counts per region
+  long long tot = 0;
+  for (long long v : w.cost) tot += v;
+  if (points) *points = tot;
+  if (point_spans) *point_spans = tot * h->n_span;
+  if (regions) *regions = (long long)w.desc.size();
+  return ISRS_EGN_OK;
+}
+
+extern "C" int isrs_egn_last_work(isrs_egn_t* h, int64_t* points, int64_t* point_spans, int64_t* regions) {
   if (!h) return fail(ISRS_EGN_EINVAL, "handle is NULL");
   if (!h->have_result) return fail(ISRS_EGN_EINVAL, "no isrs_egn_nli() result yet");
-  cudaError_t ce = cudaStreamSynchronize(h->last_stream);
-  if (ce != cudaSuccess) return cuda_fail(ce, "stream sync");
+  DeviceGuard dg(h->device);
+  cudaError_t ce = cudaEventSynchronize(h->ev[3]);
+  if (ce != cudaSuccess) return cuda_fail(ce, "event sync");
   const size_t nr = h->wl.desc.size();
   std::vector<double> np(nr);
   ce = cudaMemcpy2D(np.data(), sizeof(double), h->d_partials.p + 5, 6 * sizeof(double), sizeof(double), nr,
@@ -907,6 +1007,7 @@ extern "C" int isrs_egn_work(isrs_egn_t* h, int64_t* points, int64_t* point_span
 extern "C" int isrs_egn_last_kernel_ms(isrs_egn_t* h, double* ms_out, double* point_spans_out) {
   if (!h || !ms_out) return fail(ISRS_EGN_EINVAL, "bad argument");
   if (!h->have_result) return fail(ISRS_EGN_EINVAL, "no isrs_egn_nli() result yet");
+  DeviceGuard dg(h->device);
   cudaError_t ce = cudaEventSynchronize(h->ev[3]);
   if (ce != cudaSuccess) return cuda_fail(ce, "event sync");
   // [0] D-only launch (start of the integrand phase -> its end on st), [1] coherent launch (side
@@ -951,12 +1052,14 @@ extern "C" int isrs_egn_last_launch_count(const isrs_egn_t* h) { return h ? h->l
 extern "C" int isrs_egn_eta_host(const isrs_egn_problem* p, const isrs_egn_numerics* n, int device,
                                  int32_t n_coi, const int32_t* coi, double* eta_host, double* terms_host) {
   if (!eta_host) return fail(ISRS_EGN_EINVAL, "eta_host is NULL");
+  NvtxRange nv("isrs_egn_eta_host");
   isrs_egn_t* h = nullptr;
   int rc = isrs_egn_create(p, n, device, &h);
   if (rc) return rc;
+  DeviceGuard dg(device);
   const int nco = coi ? n_coi : p->n_ch;
   double* d = nullptr;
-  cudaError_t ce = dev_alloc(reinterpret_cast<void**>(&d), sizeof(double) * (size_t)nco * 6);
+  cudaError_t ce = dev_alloc_on(reinterpret_cast<void**>(&d), sizeof(double) * (size_t)nco * 6, nullptr);
   if (ce != cudaSuccess) {
     isrs_egn_destroy(h);
     return cuda_fail(ce, "device allocation");
@@ -968,14 +1071,15 @@ extern "C" int isrs_egn_eta_host(const isrs_egn_problem* p, const isrs_egn_numer
       ce = cudaMemcpy(terms_host, d + nco, sizeof(double) * nco * 5, cudaMemcpyDeviceToHost);
     if (ce != cudaSuccess) rc = cuda_fail(ce, "result copy");
   }
-  dev_free(d);
+  cudaStreamSynchronize(nullptr);
+  dev_free_on(d, nullptr);
   isrs_egn_destroy(h);
   return rc;
 }
 
 extern "C" void isrs_egn_destroy(isrs_egn_t* h) {
   if (!h) return;
-  cudaSetDevice(h->device);
+  DeviceGuard dg(h->device);
   cudaDeviceSynchronize();
   delete h;
 }

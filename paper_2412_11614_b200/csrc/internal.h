@@ -187,6 +187,7 @@ struct PParams {  // precompute
 
 size_t integrand_smem_bytes(int tstride, int tw, int N, bool coherent);
 int launch_precompute(const PParams& p, void* stream);
+int integrand_prepare(int mode, int tstride, int tw, int N);
 int launch_integrand(const KParams& p, const int* list, long long n_list, bool coherent,
                      void* stream, int* n_launches);
 int launch_reduce(const RParams& p, void* stream);

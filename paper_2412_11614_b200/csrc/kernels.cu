@@ -1001,11 +1001,34 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
 }
 
 template <bool COH, int MODE>
+static int set_smem(int tstride, int tw, int N) {
+  const size_t smem = integrand_smem_bytes(tstride, tw, N, COH);
+  return cudaFuncSetAttribute(integrand_kernel<COH, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem) == cudaSuccess ? 0 : -1;
+}
+
+template <int MODE>
+static int prepare_mode(int tstride, int tw, int N) {
+  return (set_smem<true, MODE>(tstride, tw, N) || set_smem<false, MODE>(tstride, tw, N)) ? -1 : 0;
+}
+
+// Dynamic shared-memory opt-in of both integrand variants of `mode`, before anything is enqueued.
+int integrand_prepare(int mode, int tstride, int tw, int N) {
+  switch (mode) {
+    case MODE_SEGMENT: return prepare_mode<MODE_SEGMENT>(tstride, tw, N);
+    case MODE_SEG32: return prepare_mode<MODE_SEG32>(tstride, tw, N);
+    case MODE_SEGDD: return prepare_mode<MODE_SEGDD>(tstride, tw, N);
+    case MODE_SEGLG: return prepare_mode<MODE_SEGLG>(tstride, tw, N);
+    case MODE_QUAD: return prepare_mode<MODE_QUAD>(tstride, tw, N);
+    case MODE_MACLAURIN: return prepare_mode<MODE_MACLAURIN>(tstride, tw, N);
+    default: return prepare_mode<MODE_UNIT>(tstride, tw, N);
+  }
+}
+
+template <bool COH, int MODE>
 static int launch_one(const KParams& p, const int* list, long long n_list, cudaStream_t st) {
   const size_t smem = integrand_smem_bytes(p.tstride, p.tw, p.N, COH);
   auto kern = integrand_kernel<COH, MODE>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return -1;
   const long long max_grid = 0x7fffffffLL;
   for (long long off = 0; off < n_list; off += max_grid) {
     const unsigned grid = (unsigned)std::min(max_grid, n_list - off);

@@ -247,6 +247,44 @@ def test_errors_surface_from_nli(isrs):
 
 # ------------------------------------------------------------------ full BASELINE sizes
 
+def _golden_files():
+    import glob
+    import os
+    here = os.path.dirname(os.path.abspath(__file__))
+    return sorted(os.path.basename(f) for f in glob.glob(os.path.join(here, "golden", "c*_eta_fastplain*.json")))
+
+
+@pytest.mark.parametrize("fname", _golden_files())
+def test_whole_eta_full_size_matches_golden(isrs, fname):
+    """North-star acceptance: whole eta (every requested COI, every region) of a BASELINE config at
+    full size through the C ABI against the fast-plain oracle's values (tests/golden/, written by
+    tests/tools/make_golden.py from oracle/ only; the fast-plain oracle is pinned to the literal
+    closed mode at <= 1e-12).  Bar: |eta_gpu - eta_oracle| / eta <= 1e-10 for every COI, the D..H
+    contributions within 1e-10 of the COI's total, exact in-support point counts."""
+    import json
+    import os
+    sys_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools")
+    import sys
+    sys.path.insert(0, sys_path)
+    from make_golden import link_hash
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", fname)) as fh:
+        g = json.load(fh)
+    link = bj_config(g["config"])
+    assert link_hash(link) == g["link_sha256"], "seeded workload drifted from the golden file"
+    e_o, t_o, n_o = np.array(g["eta"]), np.array(g["terms"]), np.array(g["points"])
+    with isrs.Engine(link) as e:
+        eta, terms = e.nli(coi=g["coi"], terms=True)
+        torch.cuda.synchronize()
+        eta, terms = eta.cpu().numpy(), terms.cpu().numpy()
+        pts = e.work()[0]
+    rel = np.abs(eta - e_o) / e_o
+    trel = np.abs(terms - t_o).max(axis=1) / np.abs(t_o).sum(axis=1)
+    print(f"{fname}: {len(e_o)} COIs, max rel eta {rel.max():.3e}, mean {rel.mean():.3e}, "
+          f"max rel terms {trel.max():.3e}")
+    assert pts == int(n_o.sum())
+    assert np.all(rel <= TOL_ETA), (fname, rel.max(), int(np.argmax(rel)))
+    assert np.all(trel <= TOL_ETA), (fname, trel.max())
+
 def theta_max(link, kappa, k1, k2):
     c = egn.canonicalize(link)
     F1, F2, _ = egn.region_points(c, kappa, k1, k2)
@@ -500,3 +538,69 @@ def test_full_size_determinism_c2(isrs):
         a = e.nli().cpu().numpy()
         b = e.nli().cpu().numpy()
     assert np.array_equal(a, b)
+
+
+def test_graph_then_direct_calls_on_other_streams(isrs):
+    """after Engine.graph() the engine keeps working on any stream, last_kernel_ms()
+    describes the last direct call, and calling the engine with another COI set does not disturb the
+    graph (it owns a private handle)."""
+    link = tiny_link(**TINY["mixed_rates_guard"])
+    ref, _ = gpu_eta(isrs, link)
+    with isrs.Engine(link) as e:
+        g = e.graph(coi=[0, 2, 4])
+        s = torch.cuda.Stream()
+        a = e.nli(stream=s)                         # all COIs: a different set than the graph's
+        b = e.nli(coi=[1, 3])                       # and another, on the default stream
+        ms, ps = e.last_kernel_ms()
+        assert ms[3] > 0 and ps[2] > 0
+        for _ in range(2):
+            eta = g.replay()
+            torch.cuda.synchronize()
+            assert np.array_equal(eta.cpu().numpy(), ref[[0, 2, 4]])
+        torch.cuda.synchronize()
+        assert np.array_equal(a.cpu().numpy(), ref)
+        assert np.array_equal(b.cpu().numpy(), ref[[1, 3]])
+        g.close()
+
+
+def test_coi_set_changes_back_to_back_without_host_sync(isrs):
+    """nli with a new COI set rebuilds its work list stream-ordered (no host or
+    device synchronisation); several different sets issued back to back on one stream, and then on a
+    second stream, each give the bitwise eta of a fresh call."""
+    link = bj_config("c1")
+    ref, tref = gpu_eta(isrs, link)
+    sets = [[0, 1, 2, 3, 4], [3], [4, 0], [2, 1, 0], [1], [0, 1, 2, 3, 4]]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    with isrs.Engine(link) as e:
+        outs = [(c, e.nli(coi=c, terms=True, stream=s1 if i % 3 else s2)) for i, c in enumerate(sets * 2)]
+        torch.cuda.synchronize()
+        for c, (eta, terms) in outs:
+            assert np.array_equal(eta.cpu().numpy(), ref[c])
+            assert np.array_equal(terms.cpu().numpy(), tref[c])
+
+
+def test_planned_work_equals_the_kernels_count(isrs):
+    """isrs_egn_work (host planner, no device) = isrs_egn_last_work (the kernels' own count)."""
+    for link, coi in ((bj_config("c1"), None), (tiny_link(**TINY["touching_bands"]), [1, 2]),
+                      (tiny_link(**TINY["mixed_rates_guard"]), None)):
+        with isrs.Engine(link) as e:
+            plan = e.planned_work(coi)
+            e.nli(coi=coi)
+            assert e.work() == plan, (plan, e.work())
+
+
+def test_capture_requires_an_existing_work_list(isrs):
+    """A call that would have to allocate (new COI set) inside a stream capture fails cleanly with
+    EINVAL instead of allocating in the graph; the handle stays usable."""
+    link = bj_config("c1")
+    ref, _ = gpu_eta(isrs, link)
+    with isrs.Engine(link) as e:
+        e.nli(coi=[0, 1])
+        s = torch.cuda.Stream()
+        out = torch.empty(1, dtype=torch.float64, device="cuda")
+        g = torch.cuda.CUDAGraph()
+        with pytest.raises(Exception):
+            with torch.cuda.graph(g, stream=s):
+                e.nli_into(out.data_ptr(), 0, [3], s.cuda_stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(e.nli(coi=[3]).cpu().numpy(), ref[[3]])

@@ -95,3 +95,53 @@ def test_gloo_two_ranks_agree_on_the_shard_plan():
         p.join(timeout=60)
     assert all(ok for _, ok, _ in res), res
     assert res[0][2] == res[1][2]
+
+
+PLANNER_LINKS = {
+    "touching_bands": dict(n_ch=4, rates_gbd=(32,), guard_ghz=0.0, n_span=2, grid_n=8, fmts=("qpsk",)),
+    "mixed_rates_guard": dict(n_ch=5, rates_gbd=(32, 64, 96), guard_ghz=12.5, n_span=2, grid_n=8,
+                              fmts=("qpsk", "16qam", "64qam")),
+    "mixed_touching": dict(n_ch=6, rates_gbd=(48, 16, 96), guard_ghz=0.0, n_span=1, grid_n=10,
+                           fmts=("qpsk",)),
+    "ragged_N34": dict(n_ch=2, rates_gbd=(68,), spacing_ghz=100.0, n_span=2, grid_n=34, fmts=("64qam",)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(PLANNER_LINKS))
+def test_planner_point_counts_equal_the_oracle(isrs, name):
+    """The host planner's exact in-support point count (closed-form per band interval of lattice lines,
+    touching bands' shared edge line counted once) equals the oracle's brute-force count per COI."""
+    from oracle import fastplain
+    link = tiny_link(**PLANNER_LINKS[name])
+    _, _, npts = fastplain.eta(link)
+    for k in range(link.n_ch):
+        _, p, _ = isrs.plan_shards(link, 1, coi=[k])
+        assert p[0] == npts[k], (name, k, p[0], npts[k])
+
+
+@pytest.mark.parametrize("golden", ["c2_eta_fastplain.json", "c5_eta_fastplain.json", "c3_eta_fastplain.json",
+                                    "c4_eta_fastplain.json"])
+def test_planner_point_counts_at_full_size(isrs, golden):
+    """Full BASELINE sizes: the planner's points per COI equal the oracle's (golden files)."""
+    import json
+    fn = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", golden)
+    if not os.path.exists(fn):
+        pytest.skip(f"{golden} not generated")
+    with open(fn) as fh:
+        g = json.load(fh)
+    link = bj_config(g["config"])
+    coi = g["coi"][:: max(1, len(g["coi"]) // 5)]
+    for k in coi:
+        _, p, _ = isrs.plan_shards(link, 1, coi=[k])
+        assert p[0] == g["points"][g["coi"].index(k)], (golden, k)
+
+
+def test_planner_is_linear_in_lines_c4():
+    """the full c4 plan (80 COIs, 345 683 regions, mixed-rate lattices) was 16.4 s
+    with a per-point walk; the per-band closed form brings it well under a second."""
+    import time
+    sys_mod = pytest.importorskip("paper_2412_11614_b200")
+    link = bj_config("c4")
+    t0 = time.perf_counter()
+    sys_mod.plan_shards(link, 1)
+    assert time.perf_counter() - t0 < 2.0
