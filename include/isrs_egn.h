@@ -195,6 +195,15 @@ ISRS_EGN_API int isrs_egn_last_kernel_ms(isrs_egn_t *h, double *ms_out, double *
  * count K_s of every span.  Spans of a chain are consecutive; sum_c G_c = n_span. */
 ISRS_EGN_API int isrs_egn_span_chains(const isrs_egn_t *h, int32_t *n_chain, int32_t *chain_g, int32_t *k_s);
 
+/* The per-span ISRS profile tables the create-time precompute kernel wrote (row a2; synchronous
+ * copy): *k_out = K_s of span `span`; ln_a_out[K] (or NULL) = ln c_k - alpha h k with
+ * c_k = x_k / (2 sinh(x_k / 2)), x_k = B_tot zeta_k, the SRS-gain normalisation of Eq. 14;
+ * zeta_out[K] (or NULL) = zeta_k = P_tot C_r L_eff(z_k) (Eq. 2) at the segment midpoints
+ * z_k = (k + 1/2) h, h = L_s / K_s (Eq. 10).  So SRS_G(z_k, f3) e^{-alpha h k} =
+ * exp(ln_a_k - zeta_k f3), the envelope the integrand kernel tabulates. */
+ISRS_EGN_API int isrs_egn_profile_tables(isrs_egn_t *h, int32_t span, int32_t *k_out, double *ln_a_out,
+                                         double *zeta_out);
+
 /* Number of kernel launches the most recent isrs_egn_nli() enqueued (for bench accounting). */
 ISRS_EGN_API int isrs_egn_last_launch_count(const isrs_egn_t *h);
 

@@ -91,5 +91,70 @@ def mu_quad(f1, f2, f, span, p_tot, b_tot, dz=None, panels_per_period=4, min_pan
     return out
 
 
+# Gauss-Kronrod 7/15 on [-1, 1] (the standard QUADPACK QK15 abscissae and weights, written from the
+# Kronrod extension of the 7-point Gauss-Legendre rule; the 7 Gauss nodes are xgk[1::2]).
+_GK15_X = np.array([0.991455371120812639206854697526329, 0.949107912342758524526189684047851,
+                    0.864864423359769072789712788640926, 0.741531185599394439863864773280788,
+                    0.586087235467691130294144845693013, 0.405845151377397166906606412076961,
+                    0.207784955007898467600689403773245, 0.0])
+_GK15_WK = np.array([0.022935322010529224963732008058970, 0.063092092629978553290700663189204,
+                     0.104790010322250183839876322541518, 0.140653259715525918745189590510238,
+                     0.169004726639267902826583426598550, 0.190350578064785409913256402421014,
+                     0.204432940075298892414161999234649, 0.209482141084727828012999174891714])
+_GK15_WG = np.array([0.129484966168869693270611432679082, 0.279705391489276667901467771423780,
+                     0.381830050505118944950369775488975, 0.417959183673469387755102040816327])
+
+
+def _gk15_nodes():
+    x = np.concatenate([-_GK15_X[:-1], _GK15_X[::-1]])               # 15 ascending nodes
+    wk = np.concatenate([_GK15_WK[:-1], _GK15_WK[::-1]])
+    wg = np.zeros(15)
+    gi = [1, 3, 5, 7, 9, 11, 13]                                       # Gauss nodes among the 15
+    wg[gi] = np.concatenate([_GK15_WG[:-1], _GK15_WG[::-1]])
+    return x, wk, wg
+
+
+def mu_quad_adaptive(f1, f2, f, span, p_tot, b_tot, dz=None, rtol=1e-13, max_panels=2_000_000):
+    """Eq. 23 by adaptive Gauss-Kronrod 7/15 (SURVEY reading C12): initial panels of at most a
+    quarter period pi/(2|chi|) of e^{i chi z} and at least 8 per span; every panel whose |K15 - G7|
+    exceeds rtol |mu| / n_panels, and is above the panel's rounding floor
+    50 eps (1 + |chi| z) int|integrand| (the phase chi z is rounded at every node), is
+    bisected until all pass.  One point at a time (pins only: an independent check of the
+    fixed-panel rule mu_quad, for |chi| L up to ~1e5 rad)."""
+    L, alpha = span["L"], span["alpha"]
+    f1 = np.atleast_1d(np.asarray(f1, dtype=np.float64))
+    f2 = np.atleast_1d(np.asarray(f2, dtype=np.float64))
+    ch = chi(f1, f2, f, span["beta2"], span["beta3"])
+    x, wk, wg = _gk15_nodes()
+    out = np.zeros(f1.shape, dtype=np.complex128)
+    for i in range(f1.size):
+        f3 = f1[i] + f2[i] - f
+        n0 = int(max(8, math.ceil(abs(ch[i]) * L / (math.pi / 2))))
+        a = np.linspace(0.0, L, n0 + 1)
+        lo, hi = a[:-1], a[1:]
+        total = 0.0 + 0.0j
+        while True:
+            mid, half = (lo + hi) / 2, (hi - lo) / 2
+            z = mid[:, None] + half[:, None] * x[None, :]
+            g = isrs.rho(z, f3, alpha, p_tot, span["cr"], b_tot) * np.exp(1j * ch[i] * z)
+            k15 = (g @ wk) * half
+            g7 = (g @ wg) * half
+            err = np.abs(k15 - g7)
+            # rounding floor: the phase chi z of every node carries ~eps |chi| z absolute error
+            floor = 50 * np.finfo(np.float64).eps * (1.0 + abs(ch[i]) * hi) * (np.abs(g) @ wk) * half
+            est = total + k15.sum()
+            bad = (err > rtol * abs(est) / max(1, lo.size)) & (err > floor)
+            total = total + k15[~bad].sum()
+            if not bad.any():
+                break
+            if lo.size > max_panels:
+                raise RuntimeError("mu_quad_adaptive: panel budget exceeded")
+            lo, hi = lo[bad], hi[bad]
+            m = (lo + hi) / 2
+            lo, hi = np.concatenate([lo, m]), np.concatenate([m, hi])
+        out[i] = total
+    return out
+
+
 MU_MODES = {"closed": mu_segment, "segment": mu_segment, "maclaurin": mu_maclaurin,
-            "quad": mu_quad}
+            "quad": mu_quad, "quad_adaptive": mu_quad_adaptive}

@@ -153,6 +153,16 @@ class Engine:
                                                  k.ctypes.data_as(_abi._ip)))
         return g[:n.value].copy(), k
 
+    def profile_tables(self, span=0):
+        """(ln_a [K], zeta [K]) of span `span`: the precompute kernel's output (row a2, Eqs. 2, 10, 14)."""
+        k = ctypes.c_int32()
+        _abi.check(_abi.get().isrs_egn_profile_tables(self._h, int(span), ctypes.byref(k), None, None))
+        la = np.zeros(k.value)
+        ze = np.zeros(k.value)
+        _abi.check(_abi.get().isrs_egn_profile_tables(self._h, int(span), ctypes.byref(k),
+                                                    la.ctypes.data_as(_abi._dp), ze.ctypes.data_as(_abi._dp)))
+        return la, ze
+
     def last_launch_count(self):
         return _abi.get().isrs_egn_last_launch_count(self._h)
 

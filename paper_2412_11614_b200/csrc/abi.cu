@@ -191,7 +191,7 @@ struct isrs_egn {
   DevBuf<double> d_Ls, d_alpha, d_gamma, d_pcr;
   double gl_x[12], gl_w[12];
   int n_chain = 0;
-  std::vector<int> chain_g, k_s;
+  std::vector<int> chain_g, k_s, cls_of_span;
   DevBuf<double> d_lnA, d_zeta;
   int kstride = 0, tstride = 0, tw = 0;
   // work list cache (last call)
@@ -486,6 +486,7 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
   }
   h->chain_g = ch_g;
   h->k_s = K;
+  h->cls_of_span = cls;
   int kmax = *std::max_element(cK.begin(), cK.end());
   int kpad = (kmax + 1) & ~1;
   h->kstride = kpad;
@@ -1044,6 +1045,24 @@ extern "C" int isrs_egn_span_chains(const isrs_egn_t* h, int32_t* n_chain, int32
     for (int c = 0; c < h->n_chain; ++c) chain_g[c] = h->chain_g[c];
   if (k_s)
     for (int s = 0; s < h->n_span; ++s) k_s[s] = h->k_s[s];
+  return ISRS_EGN_OK;
+}
+
+extern "C" int isrs_egn_profile_tables(isrs_egn_t* h, int32_t span, int32_t* k_out, double* ln_a_out,
+                                       double* zeta_out) {
+  if (!h || !k_out) return fail(ISRS_EGN_EINVAL, "bad argument");
+  if (span < 0 || span >= h->n_span) return fail(ISRS_EGN_EINVAL, "span out of range");
+  const int K = h->k_s[span];
+  *k_out = K;
+  if (!ln_a_out && !zeta_out) return ISRS_EGN_OK;
+  DeviceGuard dg(h->device);
+  if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+  const size_t off = (size_t)h->cls_of_span[span] * h->kstride;
+  cudaError_t ce = cudaSuccess;
+  if (ln_a_out) ce = cudaMemcpy(ln_a_out, h->d_lnA.p + off, sizeof(double) * K, cudaMemcpyDeviceToHost);
+  if (ce == cudaSuccess && zeta_out)
+    ce = cudaMemcpy(zeta_out, h->d_zeta.p + off, sizeof(double) * K, cudaMemcpyDeviceToHost);
+  if (ce != cudaSuccess) return cuda_fail(ce, "table copy");
   return ISRS_EGN_OK;
 }
 

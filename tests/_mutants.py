@@ -333,7 +333,27 @@ def _apply_eta_over_p_squared(fwm, isrs, link, egn):
     egn.eta = eta
 
 
+def _apply_support_bound_strict(fwm, isrs, link, egn):
+    def has_support_bound(c, kappa, k1, k2, f=None):
+        f = c.f[kappa] if f is None else f
+        lo3 = c.lo[k1] + c.lo[k2] - f + (c.delta[k1] + c.delta[k2]) / 2
+        hi3 = c.hi[k1] + c.hi[k2] - f - (c.delta[k1] + c.delta[k2]) / 2
+        return bool(np.any((c.hi > lo3) & (c.lo < hi3)))            # slip: open intervals
+    egn.has_support_bound = has_support_bound
+
+
+def _apply_support_bound_bin_edges(fwm, isrs, link, egn):
+    def has_support_bound(c, kappa, k1, k2, f=None):
+        f = c.f[kappa] if f is None else f
+        lo3 = c.lo[k1] + c.lo[k2] - f + (c.delta[k1] + c.delta[k2])   # slip: a full bin, not half
+        hi3 = c.hi[k1] + c.hi[k2] - f - (c.delta[k1] + c.delta[k2])
+        return bool(np.any((c.hi >= lo3) & (c.lo <= hi3)))
+    egn.has_support_bound = has_support_bound
+
+
 MUTANTS.update({
+    "support_bound_strict": _apply_support_bound_strict,
+    "support_bound_bin_edges": _apply_support_bound_bin_edges,
     "E_F_axes_swapped": _islands("E_F_axes_swapped"),
     "G_diagonal_difference": _islands("G_diagonal_difference"),
     "H_without_gate": _islands("H_without_gate"),

@@ -504,3 +504,38 @@ def test_c1_config_shape_and_values_finite():
     assert l.n_ch == 5 and l.grid_n == 64 and l.n_span == 1
     c = egn.canonicalize(l)
     assert abs(c.b_tot - 464e9) < 1 and abs(c.f_c - 193.4e12) < 1
+
+
+SUPPORT_LINKS = {
+    # touching bands: regions whose f3 range ends exactly on a band edge (tie points, t = 1/2)
+    "touching_32": dict(n_ch=4, rates_gbd=(32,), guard_ghz=0.0, n_span=1, grid_n=8, fmts=("qpsk",)),
+    "touching_mixed": dict(n_ch=5, rates_gbd=(48, 16, 96), guard_ghz=0.0, n_span=1, grid_n=4,
+                           fmts=("16qam",)),
+    # mixed rates with guards: a:b lattices, regions clipped at a band by one bin
+    "mixed_guard": dict(n_ch=5, rates_gbd=(32, 64, 96), guard_ghz=12.5, n_span=1, grid_n=8,
+                        fmts=("qpsk", "64qam")),
+    "uniform_spacing_eq_R": dict(n_ch=5, rates_gbd=(50,), spacing_ghz=50.0, n_span=1, grid_n=2,
+                                 fmts=("qpsk",)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(SUPPORT_LINKS))
+def test_support_bound_filter_drops_only_empty_regions(name, monkeypatch):
+    """egn.has_support_bound (a cheap necessary condition for a region to hold an island, Eq. 16
+    generalised) must never drop a region with support: eta and every D..H term with the
+    filter equal, bitwise, the brute force over every (kappa1, kappa2) pair; and the filter keeps
+    exactly the regions that have a point with f3 in some closed band (C10)."""
+    link = tiny_link(**SUPPORT_LINKS[name])
+    e1, t1 = egn.eta(link)
+    c = egn.canonicalize(link)
+    kept = {(k, a, b) for k in range(link.n_ch) for a in range(link.n_ch) for b in range(link.n_ch)
+            if egn.has_support_bound(c, k, a, b)}
+    monkeypatch.setattr(egn, "has_support_bound", lambda *a, **kw: True)
+    e2, t2 = egn.eta(link)
+    assert np.array_equal(e1, e2) and np.array_equal(t1, t2), (name, e1, e2)
+    for k in range(link.n_ch):
+        for a in range(link.n_ch):
+            for b in range(link.n_ch):
+                _, _, f3 = egn.region_points(c, k, a, b)
+                has = any(np.any((f3 >= c.lo[i]) & (f3 <= c.hi[i])) for i in range(link.n_ch))
+                assert has == ((k, a, b) in kept), (name, k, a, b, has)

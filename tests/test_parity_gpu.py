@@ -604,3 +604,27 @@ def test_capture_requires_an_existing_work_list(isrs):
                 e.nli_into(out.data_ptr(), 0, [3], s.cuda_stream)
         torch.cuda.synchronize()
         assert np.array_equal(e.nli(coi=[3]).cpu().numpy(), ref[[3]])
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c4", "c5"])
+def test_precompute_tables_match_the_oracle_profile(isrs, cfg):
+    """Row a2 on its own: the create-time precompute kernel's zeta_k (Eq. 2 at z_k, Eq. 10) and
+    ln c_k - alpha h k (Eq. 14's normalisation with the attenuation folded in) for every span class,
+    against oracle.isrs.zeta / srs_gain at the same midpoints: <= 1e-14 relative."""
+    from oracle import isrs as oisrs
+    link = bj_config(cfg)
+    c = egn.canonicalize(link)
+    with isrs.Engine(link) as e:
+        for s in range(link.n_span):
+            la, ze = e.profile_tables(s)
+            sp = c.spans[s]
+            K = fwm.segment_count(sp["L"], c.dz)
+            assert la.size == K
+            h = sp["L"] / K
+            zk = (np.arange(K) + 0.5) / K * sp["L"]
+            z_o = oisrs.zeta(zk, sp["alpha"], c.p_tot, sp["cr"])
+            # c_k = SRS_G(z_k, f3 = 0) (Eq. 14 at f3 = 0 is exactly the normalisation factor)
+            c_o = oisrs.srs_gain(zk, 0.0, sp["alpha"], c.p_tot, sp["cr"], c.b_tot)
+            assert np.all(np.abs(ze - z_o) <= 1e-14 * np.abs(z_o)), (cfg, s)
+            lna_o = np.log(c_o) - sp["alpha"] * h * np.arange(K)
+            assert np.all(np.abs(la - lna_o) <= 1e-14 * np.maximum(1.0, np.abs(lna_o))), (cfg, s)
