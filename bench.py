@@ -89,7 +89,8 @@ def ncu_traffic(config="c5"):
             with open(fn) as fh:
                 d = json.load(fh)
             for k in (d.get("kernels", []) if isinstance(d, dict) else []):
-                if "integrand_kernel<0, 0>" in (k.get("kernel") or "") and "dram_traffic_bytes" in k:
+                kn = k.get("kernel") or ""
+                if ("integrand_kernel<0, 0>" in kn or "integrand_kernel<0, 7>" in kn) and "dram_traffic_bytes" in k:
                     best = (float(k["dram_traffic_bytes"]), os.path.relpath(fn, ROOT))
         except (OSError, ValueError):
             continue
@@ -480,8 +481,9 @@ def run_ours(args, link, coi, ws, rank, local):
                               "note": "coherent launch runs concurrently on a side stream"},
                 "roofline": {"bound": "alu", "achieved": rf["ach"], "peak": rf["peak"], "unit": "TFLOP/s",
                              "frac": rf["ach"] / rf["peak"], "traffic": traffic, "traffic_source": traffic_src,
-                             "kernel": "isrs::integrand_kernel<false,0> + <true,0> (D-only and coherent "
-                                       "regions, concurrent; fork to join)",
+                             "kernel": "isrs::integrand_kernel<false,MODE> + <true,MODE> (D-only and coherent "
+                                       "regions, concurrent; fork to join; MODE 7 = segment mode with chain "
+                                       "groups when a group of identical spans holds > 1 chain, else 0)",
                              "flops_per_point_span": rf["fpp"],
                              "span_chains": [int(g) for g in rf["chain_g"]],
                              "peak_note": ("derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz "

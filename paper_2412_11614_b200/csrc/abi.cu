@@ -186,11 +186,11 @@ struct isrs_egn {
   DevBuf<double> d_lo, d_hi, d_f, d_G, d_R, d_P, d_phi, d_psi, d_delta;
   DevBuf<long long> d_rate;
   DevBuf<double> d_A2, d_A3, d_Eh, d_ah, d_gh, d_macc, d_aL;
-  DevBuf<int> d_K, d_cls, d_Kc, d_chain_s0, d_chain_g;
+  DevBuf<int> d_K, d_cls, d_Kc, d_chain_s0, d_chain_g, d_grp_c0;
   DevBuf<double> d_lnc_L, d_zeta_L, d_lgA, d_lgB, d_lgC, d_lgD;
   DevBuf<double> d_Ls, d_alpha, d_gamma, d_pcr;
   double gl_x[12], gl_w[12];
-  int n_chain = 0;
+  int n_chain = 0, n_grp = 0;
   std::vector<int> chain_g, k_s, cls_of_span;
   DevBuf<double> d_lnA, d_zeta;
   int kstride = 0, tstride = 0, tw = 0;
@@ -459,6 +459,24 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
     }
   }
   h->n_chain = (int)ch_s0.size();
+  // chain groups (fp64 segment mode with chaining): consecutive chains whose spans are identical,
+  // every chain but the group's last of the same length G (the cap split)
+  std::vector<int> grp_c0;
+  const bool group_ok = chain_ok && num.precision == 64 &&
+                        !(num.flags & (ISRS_EGN_FLAG_DEDUP | ISRS_EGN_FLAG_LITERAL_GAIN));
+  for (int c = 0; c < h->n_chain; ++c) {
+    bool join = false;
+    if (group_ok && c > 0) {
+      const int s = ch_s0[c], r = ch_s0[c - 1];
+      join = p->length_m[s] == p->length_m[r] && p->alpha_per_m[s] == p->alpha_per_m[r] &&
+             p->beta2_s2_per_m[s] == p->beta2_s2_per_m[r] && p->beta3_s3_per_m[s] == p->beta3_s3_per_m[r] &&
+             p->gamma_per_w_m[s] == p->gamma_per_w_m[r] && p->cr_per_w_m_hz[s] == p->cr_per_w_m_hz[r] &&
+             ch_g[c - 1] == ch_g[grp_c0.back()];
+    }
+    if (!join) grp_c0.push_back(c);
+  }
+  h->n_grp = (int)grp_c0.size();
+  grp_c0.push_back(h->n_chain);
   // ---- literal gain products (NEXT-4b): SRS gain at each span end, prefix / suffix sums
   const int ns = p->n_span;
   std::vector<double> lncL(ns), zL(ns), lgA(ns, 0.0), lgB(ns, 0.0), lgC(ns, 0.0), lgD(ns, 0.0);
@@ -497,7 +515,7 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
     delete h;
     return fail(ISRS_EGN_ERANGE, "K_s too large for the shared-memory envelope table (reduce K or raise dz)");
   }
-  const size_t smem = integrand_smem_bytes(h->tstride, h->tw, N, true);
+  const size_t smem = integrand_smem_bytes(h->tstride, h->tw, N, true, true);
   if (smem > 220 * 1024) {
     delete h;
     return fail(ISRS_EGN_ERANGE, "grid_n / K_s exceed the shared-memory budget");
@@ -510,6 +528,7 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
   pk.add(&h->d_A3, A3); pk.add(&h->d_Eh, Eh); pk.add(&h->d_ah, ah); pk.add(&h->d_gh, gh);
   pk.add(&h->d_macc, macc); pk.add(&h->d_aL, aL); pk.add(&h->d_K, K); pk.add(&h->d_cls, cls);
   pk.add(&h->d_Kc, cK); pk.add(&h->d_chain_s0, ch_s0); pk.add(&h->d_chain_g, ch_g);
+  pk.add(&h->d_grp_c0, grp_c0);
   pk.add(&h->d_lnc_L, lncL); pk.add(&h->d_zeta_L, zL); pk.add(&h->d_lgA, lgA); pk.add(&h->d_lgB, lgB);
   pk.add(&h->d_lgC, lgC); pk.add(&h->d_lgD, lgD); pk.add(&h->d_Ls, vL); pk.add(&h->d_alpha, vA);
   pk.add(&h->d_gamma, vG); pk.add(&h->d_pcr, vP); pk.add(&dL, cL); pk.add(&dA, cA); pk.add(&dC, cC);
@@ -737,7 +756,8 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
                    : (h->num.mu_mode == ISRS_EGN_MU_MACLAURIN ? MODE_MACLAURIN
                       : (h->num.precision == 32 ? MODE_SEG32
                          : ((h->num.flags & ISRS_EGN_FLAG_DEDUP) ? MODE_SEGDD
-                            : ((h->num.flags & ISRS_EGN_FLAG_LITERAL_GAIN) ? MODE_SEGLG : MODE_SEGMENT)))));
+                            : ((h->num.flags & ISRS_EGN_FLAG_LITERAL_GAIN) ? MODE_SEGLG
+                               : (h->n_grp < h->n_chain ? MODE_SEGGRP : MODE_SEGMENT))))));
   if (integrand_prepare(mode, h->tstride, h->tw, h->N) != 0)
     return cuda_fail(cudaGetLastError(), "integrand kernel attributes");
   // calls on one handle share its partials (and a rebuild frees the previous work list): a call on
@@ -808,6 +828,7 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
   kp.mac_c = h->d_macc.p; kp.aL = h->d_aL.p; kp.K = h->d_K.p; kp.cls = h->d_cls.p;
   kp.n_span = h->n_span;
   kp.chain_s0 = h->d_chain_s0.p; kp.chain_g = h->d_chain_g.p; kp.n_chain = h->n_chain;
+  kp.grp_c0 = h->d_grp_c0.p; kp.n_grp = h->n_grp;
   kp.lnc_L = h->d_lnc_L.p; kp.zeta_L = h->d_zeta_L.p; kp.lgA = h->d_lgA.p; kp.lgB = h->d_lgB.p;
   kp.lgC = h->d_lgC.p; kp.lgD = h->d_lgD.p;
   kp.Ls = h->d_Ls.p; kp.alpha = h->d_alpha.p; kp.gamma = h->d_gamma.p; kp.pcr = h->d_pcr.p;

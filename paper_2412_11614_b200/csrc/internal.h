@@ -70,8 +70,9 @@ enum : int { NEED_E = 1, NEED_F = 2, NEED_G = 4, NEED_H = 8, FV_SHIFT = 8 };
 // factor; fp64 chi h and its exact reduction, the phase advance and every accumulation)
 // MODE_SEGDD: the segment form with span-class dedup (NEXT-4a, ISRS_EGN_FLAG_DEDUP)
 // MODE_SEGLG: the segment form with the literal gain products of Eq. 22 (NEXT-4b)
+// MODE_SEGGRP: MODE_SEGMENT with chain groups (some group of identical spans holds > 1 chain, R9)
 enum : int { MODE_SEGMENT = 0, MODE_MACLAURIN = 1, MODE_UNIT = 2, MODE_SEG32 = 3, MODE_SEGDD = 4,
-             MODE_SEGLG = 5, MODE_QUAD = 6 };
+             MODE_SEGLG = 5, MODE_QUAD = 6, MODE_SEGGRP = 7 };
 
 struct RegionDesc {
   int kappa, k1, k2, flags;
@@ -107,6 +108,12 @@ struct KParams {
   const int* chain_s0;
   const int* chain_g;
   int n_chain;
+  // chain groups (MODE_SEGMENT): runs of consecutive chains of identical spans (a chain split only by
+  // the CHAIN_MAX cap); group g covers chains [grp_c0[g], grp_c0[g + 1]).  Their z = e^{i chi h} and
+  // I_0 are formed once per group and the chains' segment sums are combined with their span phases
+  // before the single mu = I_0 S multiply (reading R9).  Other modes: one chain per group.
+  const int* grp_c0;
+  int n_grp;
   // literal gain (NEXT-4b): ln S_s(x) = lnc_L[s] - zeta_L[s] x is the SRS gain at the end of span s;
   // ln Lambda_s = (lgA - lgB (f1+f2+f3)) / 2 + (lgC - lgD f) / 2 with prefix (A, B) / suffix (C, D) sums
   const double* lnc_L;
@@ -185,7 +192,7 @@ struct PParams {  // precompute
   double* zeta;
 };
 
-size_t integrand_smem_bytes(int tstride, int tw, int N, bool coherent);
+size_t integrand_smem_bytes(int tstride, int tw, int N, bool coherent, bool grouped);
 int launch_precompute(const PParams& p, void* stream);
 int integrand_prepare(int mode, int tstride, int tw, int N);
 int launch_integrand(const KParams& p, const int* list, long long n_list, bool coherent,

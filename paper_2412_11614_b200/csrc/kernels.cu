@@ -104,11 +104,13 @@ struct Smem {
   double2* colacc;   // [N]
   double2* lineacc;  // [LINE_CAP]
   double* wF;        // [LINE_CAP] sum_t t [k3 == k2]
+  double* gst;       // [5 PPT][BLOCK] per-thread chain-group state: (f1-f)(f2-f), f1+f2, chi h / pi,
+                     // e^{i G chi L} (re, im)
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
-__host__ __device__ inline size_t smem_layout(int tstride, int tw, int N, bool coh, char* base,
+__host__ __device__ inline size_t smem_layout(int tstride, int tw, int N, bool coh, bool grp, char* base,
                                               Smem* s) {
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -124,6 +126,7 @@ __host__ __device__ inline size_t smem_layout(int tstride, int tw, int N, bool c
   size_t oD = take(sizeof(double) * LINE_CAP);
   size_t oE = take(sizeof(double) * LINE_CAP);
   size_t oW = take(sizeof(double) * LINE_CAP);
+  size_t oG = grp ? take(sizeof(double) * 5 * PPT * BLOCK) : 0;
   size_t oC = take(sizeof(int4) * (BLOCK / 32 + 1));
   size_t oR = take(sizeof(double) * BLOCK);
   size_t oY = 0, oRow = 0, oCol = 0, oLine = 0;
@@ -142,6 +145,7 @@ __host__ __device__ inline size_t smem_layout(int tstride, int tw, int N, bool c
     s->wD = (double*)(base + oD);
     s->wE = (double*)(base + oE);
     s->wF = (double*)(base + oW);
+    s->gst = grp ? (double*)(base + oG) : nullptr;
     s->scan = (int*)(base + oC);
     s->red = (double*)(base + oR);
     s->ybuf = coh ? (double2*)(base + oY) : nullptr;
@@ -152,8 +156,8 @@ __host__ __device__ inline size_t smem_layout(int tstride, int tw, int N, bool c
   return off;
 }
 
-size_t integrand_smem_bytes(int tstride, int tw, int N, bool coherent) {
-  return smem_layout(tstride, tw, N, coherent, nullptr, nullptr);
+size_t integrand_smem_bytes(int tstride, int tw, int N, bool coherent, bool grouped) {
+  return smem_layout(tstride, tw, N, coherent, grouped, nullptr, nullptr);
 }
 
 // Block-wide exclusive scan of an int triple (w unused); returns totals.  All threads must call.
@@ -671,6 +675,47 @@ __device__ __forceinline__ void span_seg32(const KParams& p, int ch, int G, int 
   }
 }
 
+// The segment sum of one span chain (Eqs. 8-9 with I_k = I_0 w^k, reading R2 / R9): the chain's G
+// spans walk the thread's envelope row G times (rowp[npair] repeats rowp[0] for the wrap) through the
+// second-order recurrence b_k = (2cos(chi h) b_{k+1} + a'_k) - b_{k+2}, 1 DFMA + 1 DADD per segment,
+// PPT independent recurrences interleaved; returns sum_k a'_k z^k = a'_0 + z b_1 - b_2 per point.
+__device__ __forceinline__ void chain_sum(const double2* __restrict__ rowp, int npair, int G,
+                                          const double (&c2)[PPT], const double (&sn)[PPT],
+                                          double (&accr)[PPT], double (&acci)[PPT]) {
+  double b1[PPT], b2[PPT];
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    b1[q] = 0.0;
+    b2[q] = 0.0;
+  }
+  double2 tc = rowp[0];
+  for (int gi = 0; gi < G; ++gi) {
+    const int nit = (gi == G - 1) ? npair - 1 : npair;
+    ISRS_UNROLL_PRAGMA(ISRS_UNROLL)
+    for (int i2 = 0; i2 < nit; ++i2) {
+      const double2 tn = rowp[i2 + 1];
+      // the coefficient a'_k, shared by the PPT recurrences, sits in the DFMA's addend slot where
+      // the operand-reuse cache serves it (tools/fp64_pattern_probe.cu B26)
+      double n0[PPT];
+#pragma unroll
+      for (int q = 0; q < PPT; ++q) n0[q] = fma(c2[q], b1[q], tc.x) - b2[q];
+#pragma unroll
+      for (int q = 0; q < PPT; ++q) {
+        const double n1 = fma(c2[q], n0[q], tc.y) - b1[q];
+        b2[q] = n0[q];
+        b1[q] = n1;
+      }
+      tc = tn;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const double n0 = fma(c2[q], b1[q], tc.x) - b2[q];   // b_1
+    accr[q] = fma(0.5 * c2[q], n0, tc.y - b1[q]);        // a'_0 + z b_1 - b_2, cos(chi h) = c2 / 2
+    acci[q] = sn[q] * n0;
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // integrand (rows a3-a6)
 
@@ -678,11 +723,13 @@ template <bool COH, int MODE>
 __global__ void __launch_bounds__(BLOCK, MIN_BLOCKS)
 integrand_kernel(const KParams p, const int* __restrict__ list) {
   extern __shared__ __align__(16) char smem_raw[];
-  constexpr bool SEGM = (MODE == MODE_SEGMENT || MODE == MODE_SEGDD || MODE == MODE_SEGLG);
+  constexpr bool SEGM = (MODE == MODE_SEGMENT || MODE == MODE_SEGDD || MODE == MODE_SEGLG || MODE == MODE_SEGGRP);
   constexpr bool LG = (MODE == MODE_SEGLG);   // literal Eq. 22 gain products (NEXT-4b)
   constexpr bool DEDUP = (MODE == MODE_SEGDD);
   Smem sm;
-  smem_layout(p.tstride, p.tw, p.N, COH, smem_raw, &sm);
+  constexpr bool grouped = (MODE == MODE_SEGGRP);   // chain groups (R9): the segment mode when some
+                                                     // group holds more than one chain
+  smem_layout(p.tstride, p.tw, p.N, COH, grouped, smem_raw, &sm);
   const int tid = threadIdx.x;
   PROF_DECL
   const int rid = list[blockIdx.x];
@@ -782,6 +829,10 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
         const double u = __dadd_rn(f1, -f), w = __dadd_rn(f2, -f);
         uv[q] = __dmul_rn(u, w);
         Ssum[q] = __dadd_rn(f1, f2);
+        if constexpr (grouped) {                    // chain groups read them from smem (register room)
+          sm.gst[q * BLOCK + tid] = uv[q];
+          sm.gst[(PPT + q) * BLOCK + tid] = Ssum[q];
+        }
       }
 
       double yr[PPT], yi[PPT], th[PPT];
@@ -793,7 +844,100 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
       }
 
       PROF_MARK(2)   // chunk setup (line lookup, geometry)
-      if (MODE != MODE_UNIT) {
+      if constexpr (grouped) {
+        // ---- chain groups (reading R9): z = e^{i chi h} and I_0 once per group of identical spans;
+        // each chain's segment sum is rotated by its span phase e^{i theta_c} (Eq. 22, C3) and summed,
+        // then mu = gamma I_0 S once per group
+        for (int gr = 0; gr < p.n_grp; ++gr) {
+          if (gr > 0) { PROF_MARK(4) }
+          const int c0 = __ldg(p.grp_c0 + gr), c1 = __ldg(p.grp_c0 + gr + 1);
+          const int s = __ldg(p.chain_s0 + c0);
+          const int cls = __ldg(p.cls + s);
+          if (cls != tcls || i_first < tb || i_last >= tb + tn) {
+            __syncthreads();
+            tb = i_first;
+            tn = (p.n_cls == 1) ? min(p.tw, S - i_first) : (i_last - i_first + 1);
+            tcls = cls;
+            build_table<false>(p, sm, cls, tb, tn, C, g);
+            PROF_COUNT(8, 1)
+            PROF_COUNT(9, tn)
+            __syncthreads();
+          }
+          PROF_MARK(3)
+          if (!wact) continue;   // warp-uniform: idle warps of a ragged last chunk skip the math
+          const double A2 = __ldg(p.A2 + s), A3 = __ldg(p.A3 + s);
+          const int Ks = __ldg(p.K + s);
+          const int npair = ((__ldg(p.Kc + cls) + 1) & ~1) >> 1;
+          ISRS_BOUND(li - tb, tn);
+          const double2* rowp = (const double2*)(sm.T + (li - tb) * p.tstride);
+          // thread-private smem slots (column tid: conflict-free) hold what is only needed between
+          // chains, so the recurrence runs with the register budget of a single chain
+          double* gu = sm.gst + tid;                        // [q * BLOCK]: (f1 - f)(f2 - f)
+          double* gs = sm.gst + PPT * BLOCK + tid;          // f1 + f2
+          double* gx = sm.gst + 2 * PPT * BLOCK + tid;      // chi h / pi
+          double* gwr = sm.gst + 3 * PPT * BLOCK + tid;     // w = e^{i G0 chi L}, real
+          double* gwi = sm.gst + 4 * PPT * BLOCK + tid;     // imaginary
+          const int nch = c1 - c0, G0 = __ldg(p.chain_g + c0);
+          double c2[PPT], sn[PPT], sr[PPT], si[PPT];
+#pragma unroll
+          for (int q = 0; q < PPT; ++q) {
+            const double x = gu[q * BLOCK] * fma(A3, gs[q * BLOCK], A2);   // chi h / pi (Eq. 5 x h / pi)
+            gx[q * BLOCK] = x;
+            double cs;
+            sincospi_d(x, &sn[q], &cs);                     // z = e^{i chi h}
+            c2[q] = cs + cs;
+            if (nch > 1) {                                   // w = z^{G0 K} = e^{i G0 chi L}
+              const double t = x * (double)(Ks * G0);
+              double ss, cc;
+              sincospi_d(t - 2.0 * rint(0.5 * t), &ss, &cc);
+              gwr[q * BLOCK] = cc;
+              gwi[q * BLOCK] = ss;
+            }
+          }
+          // S = sum_c e^{i (theta_c - theta_c0)} sum_c = A_c0 + w (A_c0+1 + w (...)), chains of the
+          // group in reverse (Horner over the chains; every chain but the last has G0 spans)
+          for (int ch = c1 - 1; ch >= c0; --ch) {
+            double accr[PPT], acci[PPT];
+            chain_sum(rowp, npair, __ldg(p.chain_g + ch), c2, sn, accr, acci);
+            if (ch == c1 - 1) {
+#pragma unroll
+              for (int q = 0; q < PPT; ++q) {
+                sr[q] = accr[q];
+                si[q] = acci[q];
+              }
+            } else {
+#pragma unroll
+              for (int q = 0; q < PPT; ++q) {
+                const double a = gwr[q * BLOCK], b = gwi[q * BLOCK];
+                const double t = fma(sr[q], a, fma(-si[q], b, accr[q]));
+                si[q] = fma(sr[q], b, fma(si[q], a, acci[q]));
+                sr[q] = t;
+              }
+            }
+          }
+          const double Eh = __ldg(p.Eh + s), ah = __ldg(p.ah + s), gh = __ldg(p.gh + s);
+          int gsum = 0;
+          for (int ch = c0; ch < c1; ++ch) gsum += __ldg(p.chain_g + ch);
+#pragma unroll
+          for (int q = 0; q < PPT; ++q) {
+            const double x = gx[q * BLOCK];
+            const double px = CUDART_PI * x;     // chi h
+            // I_0 = (w - 1)/(i chi - alpha) = h (w - 1) conj(d) / |d|^2, d = -alpha h + i chi h
+            const double wr1 = fma(Eh, 0.5 * c2[q], -1.0), wi = Eh * sn[q];
+            const double inv = gh * rcp_d(fma(px, px, ah * ah));   // gamma_s h / |d|^2
+            const double nr = fma(wi, px, -ah * wr1);
+            const double ni = -fma(px, wr1, ah * wi);
+            const double mr = (nr * sr[q] - ni * si[q]) * inv;     // gamma mu_group / e^{i theta_c0}
+            const double mi = (nr * si[q] + ni * sr[q]) * inv;
+            double ps = 0.0, pc = 1.0;                             // theta_1 = 0 for the first group
+            if (gr > 0) sincospi_d(th[q], &ps, &pc);
+            yr[q] = fma(mr, pc, fma(-mi, ps, yr[q]));              // Y += gamma mu e^{i theta} (Eq. 22, C3)
+            yi[q] = fma(mr, ps, fma(mi, pc, yi[q]));
+            const double t2 = fma(x, (double)(Ks * gsum), th[q]);  // theta += chi L per span of the group
+            th[q] = t2 - 2.0 * rint(0.5 * t2);
+          }
+        }
+      } else if constexpr (MODE != MODE_UNIT) {
         for (int ch = 0; ch < p.n_chain; ++ch) {
           if (ch > 0) { PROF_MARK(4) }   // previous chain's span math
           // chain of G identical consecutive spans starting at s (G = 1 unless chained, R9)
@@ -1002,7 +1146,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
 
 template <bool COH, int MODE>
 static int set_smem(int tstride, int tw, int N) {
-  const size_t smem = integrand_smem_bytes(tstride, tw, N, COH);
+  const size_t smem = integrand_smem_bytes(tstride, tw, N, COH, MODE == MODE_SEGGRP);
   return cudaFuncSetAttribute(integrand_kernel<COH, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)smem) == cudaSuccess ? 0 : -1;
 }
@@ -1016,6 +1160,7 @@ static int prepare_mode(int tstride, int tw, int N) {
 int integrand_prepare(int mode, int tstride, int tw, int N) {
   switch (mode) {
     case MODE_SEGMENT: return prepare_mode<MODE_SEGMENT>(tstride, tw, N);
+    case MODE_SEGGRP: return prepare_mode<MODE_SEGGRP>(tstride, tw, N);
     case MODE_SEG32: return prepare_mode<MODE_SEG32>(tstride, tw, N);
     case MODE_SEGDD: return prepare_mode<MODE_SEGDD>(tstride, tw, N);
     case MODE_SEGLG: return prepare_mode<MODE_SEGLG>(tstride, tw, N);
@@ -1027,7 +1172,7 @@ int integrand_prepare(int mode, int tstride, int tw, int N) {
 
 template <bool COH, int MODE>
 static int launch_one(const KParams& p, const int* list, long long n_list, cudaStream_t st) {
-  const size_t smem = integrand_smem_bytes(p.tstride, p.tw, p.N, COH);
+  const size_t smem = integrand_smem_bytes(p.tstride, p.tw, p.N, COH, MODE == MODE_SEGGRP);
   auto kern = integrand_kernel<COH, MODE>;
   const long long max_grid = 0x7fffffffLL;
   for (long long off = 0; off < n_list; off += max_grid) {
@@ -1044,6 +1189,7 @@ int launch_integrand(const KParams& p, const int* list, long long n_list, bool c
   *n_launches += 1;
   if (coherent) {
     if (p.mode == MODE_SEGMENT) return launch_one<true, MODE_SEGMENT>(p, list, n_list, st);
+    if (p.mode == MODE_SEGGRP) return launch_one<true, MODE_SEGGRP>(p, list, n_list, st);
     if (p.mode == MODE_SEG32) return launch_one<true, MODE_SEG32>(p, list, n_list, st);
     if (p.mode == MODE_SEGDD) return launch_one<true, MODE_SEGDD>(p, list, n_list, st);
     if (p.mode == MODE_SEGLG) return launch_one<true, MODE_SEGLG>(p, list, n_list, st);
@@ -1052,6 +1198,7 @@ int launch_integrand(const KParams& p, const int* list, long long n_list, bool c
     return launch_one<true, MODE_UNIT>(p, list, n_list, st);
   }
   if (p.mode == MODE_SEGMENT) return launch_one<false, MODE_SEGMENT>(p, list, n_list, st);
+  if (p.mode == MODE_SEGGRP) return launch_one<false, MODE_SEGGRP>(p, list, n_list, st);
   if (p.mode == MODE_SEG32) return launch_one<false, MODE_SEG32>(p, list, n_list, st);
   if (p.mode == MODE_SEGDD) return launch_one<false, MODE_SEGDD>(p, list, n_list, st);
   if (p.mode == MODE_SEGLG) return launch_one<false, MODE_SEGLG>(p, list, n_list, st);
