@@ -43,20 +43,29 @@ def fp64_peak_tflops(mhz=SM_MAX_MHZ):
     return SMS * FP64_LANES * 2 * mhz * 1e6 / 1e12
 
 
-def algorithmic_work_per_point(chain_g, k_s):
+def algorithmic_work_per_point(chain_g, k_s, grp_c0=None):
     """Algorithmic FP64 work per grid point summed over the link, given the span
     chains (reading R9): a chain of G spans with K segments (K_p = K rounded up to even) runs
     one second-order recurrence over G*K_p segments, 1 DFMA + 1 DADD each = 3 flops / 2 FP64
-    pipe slots (the first step is a bare add: -3 / -2), plus 40 flops / 25 slots of per-chain
-    arithmetic (chi, 2cos, I_0, mu, Y accumulation, phase advance); the two sincospi and the
-    reciprocal seed per chain are not counted.  Returns (flops, fp64 pipe slots)."""
-    flops = slots = 0.0
-    s = 0
+    pipe slots (the first step is a bare add: -3 / -2); each chain GROUP (grp_c0: bounds of runs of
+    chains of identical spans; default one chain per group) adds 40 flops / 25 slots of arithmetic
+    (chi, 2cos, I_0, mu, Y accumulation, phase advance) and each chain after a group's first one 8
+    flops / 4 slots (its complex Horner step); the sincospi and reciprocal seeds are not counted.
+    Returns (flops, fp64 pipe slots)."""
+    starts = [0]
     for g in chain_g:
-        kp = 2 * ((int(k_s[s]) + 1) // 2)
-        flops += 3 * (g * kp - 1) + 40
-        slots += 2 * (g * kp - 1) + 25
-        s += g
+        starts.append(starts[-1] + int(g))
+    if grp_c0 is None:
+        grp_c0 = list(range(len(chain_g) + 1))
+    flops = slots = 0.0
+    for gi in range(len(grp_c0) - 1):
+        c0, c1 = int(grp_c0[gi]), int(grp_c0[gi + 1])
+        flops += 40 + 8 * (c1 - c0 - 1)
+        slots += 25 + 4 * (c1 - c0 - 1)
+        for c in range(c0, c1):
+            kp = 2 * ((int(k_s[starts[c]]) + 1) // 2)
+            flops += 3 * (int(chain_g[c]) * kp - 1)
+            slots += 2 * (int(chain_g[c]) * kp - 1)
     return flops, slots
 
 
@@ -274,14 +283,15 @@ def roofline_of(eng, link, kern_ms, precision):
     ki_ms = float(np.mean([k[0][3] for k in kern_ms]))
     ps_i = kern_ms[-1][1][2]
     chain_g, k_s = eng.span_chains()
-    fpp, spp = (v / link.n_span for v in algorithmic_work_per_point(chain_g, k_s))  # per point-span
+    grp_c0 = eng.chain_groups() if precision == 64 else None
+    fpp, spp = (v / link.n_span for v in algorithmic_work_per_point(chain_g, k_s, grp_c0))  # per point-span
     ach = ps_i * fpp / (ki_ms * 1e-3) / 1e12
     # fp64: 64 FP64 FMA lanes per SM; the mixed fp32 variant (a8) runs its recurrence on the
     # 128 FP32 FMA lanes per SM, so its roofline takes the FP32 peak (2x)
     peak = fp64_peak_tflops() * (2.0 if precision == 32 else 1.0)
     slots_ach = ps_i * spp / (ki_ms * 1e-3) / 1e12
     slots_peak = SMS * FP64_LANES * SM_MAX_MHZ * 1e6 / 1e12
-    return dict(ki_ms=ki_ms, ps_i=ps_i, chain_g=chain_g, k_s=k_s, fpp=fpp, spp=spp, ach=ach, peak=peak,
+    return dict(ki_ms=ki_ms, ps_i=ps_i, chain_g=chain_g, k_s=k_s, grp_c0=grp_c0, fpp=fpp, spp=spp, ach=ach, peak=peak,
                 slots_ach=slots_ach, slots_peak=slots_peak)
 
 
@@ -486,6 +496,7 @@ def run_ours(args, link, coi, ws, rank, local):
                                        "groups when a group of identical spans holds > 1 chain, else 0)",
                              "flops_per_point_span": rf["fpp"],
                              "span_chains": [int(g) for g in rf["chain_g"]],
+                             "chain_groups": [int(g) for g in rf["grp_c0"]] if rf["grp_c0"] is not None else None,
                              "peak_note": ("derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz "
                                            "(tools/dmma_probe.cu: a DFMA stream reaches 128 flop/SM-cycle = this peak)"
                                            if args.precision == 64 else

@@ -204,6 +204,12 @@ ISRS_EGN_API int isrs_egn_span_chains(const isrs_egn_t *h, int32_t *n_chain, int
 ISRS_EGN_API int isrs_egn_profile_tables(isrs_egn_t *h, int32_t span, int32_t *k_out, double *ln_a_out,
                                          double *zeta_out);
 
+/* Chain groups of the handle (reading R9, fp64 segment mode): runs of consecutive chains of identical
+ * spans whose z = e^{i chi h} and I_0 the integrand forms once; group g covers chains
+ * [grp_c0[g], grp_c0[g + 1]).  *n_grp receives the count; grp_c0 (or NULL, capacity n_span + 1) the
+ * bounds.  Other modes: one chain per group.  (For the bench's algorithmic flop count.) */
+ISRS_EGN_API int isrs_egn_chain_groups(const isrs_egn_t *h, int32_t *n_grp, int32_t *grp_c0);
+
 /* Number of kernel launches the most recent isrs_egn_nli() enqueued (for bench accounting). */
 ISRS_EGN_API int isrs_egn_last_launch_count(const isrs_egn_t *h);
 

@@ -153,6 +153,13 @@ class Engine:
                                                  k.ctypes.data_as(_abi._ip)))
         return g[:n.value].copy(), k
 
+    def chain_groups(self):
+        """Bounds [n_grp + 1] of the chain groups (R9): group g covers chains grp_c0[g] .. grp_c0[g+1]-1."""
+        n = ctypes.c_int32()
+        g = np.zeros(self.n_span + 1, dtype=np.int32)
+        _abi.check(_abi.get().isrs_egn_chain_groups(self._h, ctypes.byref(n), g.ctypes.data_as(_abi._ip)))
+        return g[:n.value + 1].copy()
+
     def profile_tables(self, span=0):
         """(ln_a [K], zeta [K]) of span `span`: the precompute kernel's output (row a2, Eqs. 2, 10, 14)."""
         k = ctypes.c_int32()

@@ -191,7 +191,7 @@ struct isrs_egn {
   DevBuf<double> d_Ls, d_alpha, d_gamma, d_pcr;
   double gl_x[12], gl_w[12];
   int n_chain = 0, n_grp = 0;
-  std::vector<int> chain_g, k_s, cls_of_span;
+  std::vector<int> chain_g, k_s, cls_of_span, grp_c0;
   DevBuf<double> d_lnA, d_zeta;
   int kstride = 0, tstride = 0, tw = 0;
   // work list cache (last call)
@@ -477,6 +477,7 @@ extern "C" int isrs_egn_create(const isrs_egn_problem* p, const isrs_egn_numeric
   }
   h->n_grp = (int)grp_c0.size();
   grp_c0.push_back(h->n_chain);
+  h->grp_c0 = grp_c0;
   // ---- literal gain products (NEXT-4b): SRS gain at each span end, prefix / suffix sums
   const int ns = p->n_span;
   std::vector<double> lncL(ns), zL(ns), lgA(ns, 0.0), lgB(ns, 0.0), lgC(ns, 0.0), lgD(ns, 0.0);
@@ -1084,6 +1085,14 @@ extern "C" int isrs_egn_profile_tables(isrs_egn_t* h, int32_t span, int32_t* k_o
   if (ce == cudaSuccess && zeta_out)
     ce = cudaMemcpy(zeta_out, h->d_zeta.p + off, sizeof(double) * K, cudaMemcpyDeviceToHost);
   if (ce != cudaSuccess) return cuda_fail(ce, "table copy");
+  return ISRS_EGN_OK;
+}
+
+extern "C" int isrs_egn_chain_groups(const isrs_egn_t* h, int32_t* n_grp, int32_t* grp_c0) {
+  if (!h || !n_grp) return fail(ISRS_EGN_EINVAL, "bad argument");
+  *n_grp = h->n_grp;
+  if (grp_c0)
+    for (int g = 0; g <= h->n_grp; ++g) grp_c0[g] = h->grp_c0[g];
   return ISRS_EGN_OK;
 }
 

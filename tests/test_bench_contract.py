@@ -53,6 +53,9 @@ def test_roofline_unit_counts():
     # odd K pads to even; unchained spans count one chain each
     assert bench.algorithmic_work_per_point([1, 1], [73, 81]) == (3 * 73 + 40 + 3 * 81 + 40,
                                                                   2 * 73 + 25 + 2 * 81 + 25)
+    # chain groups (c5: 5 chains of 10 spans, one group): one 40-flop epilogue + 4 Horner steps of 8
+    assert bench.algorithmic_work_per_point([10] * 5, [80] * 50, [0, 5]) == (5 * 3 * 799 + 40 + 4 * 8,
+                                                                             5 * 2 * 799 + 25 + 4 * 4)
 
 
 @pytest.mark.parametrize("cfg", ["c2", "c5"])
