@@ -193,7 +193,9 @@ __device__ inline int4 block_scan3(int4 v, int* scratch, int4* total) {
   return make_int4(base.x + x.x - v.x, base.y + x.y - v.y, base.z + x.z - v.z, 0);
 }
 
-// Fixed-tree block sum (deterministic).  All threads must call.
+// Fixed-tree block sum (deterministic) through shared memory; the D-only kernel's once-per-region
+// sum (its register allocation, hence the recurrence's schedule, is tuned with this form).  All
+// threads must call.
 __device__ inline double block_sum(double v, double* red) {
   red[threadIdx.x] = v;
   __syncthreads();
@@ -205,6 +207,30 @@ __device__ inline double block_sum(double v, double* red) {
   double r = red[0];
   __syncthreads();
   return r;
+}
+
+// Deterministic block sums of NV values (all threads must call; every thread gets the totals): a
+// butterfly of warp shuffles (xor 16, 8, 4, 2, 1 -- a fixed tree, so bitwise reproducible) inside each
+// warp, then the BLOCK/32 warp partials added in warp order from shared memory.
+template <int NV>
+__device__ inline void block_sum_n(double (&v)[NV], double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) red[NV * warp + k] = v[k];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double t = red[k];
+#pragma unroll
+    for (int w = 1; w < BLOCK / 32; ++w) t += red[NV * w + k];
+    v[k] = t;
+  }
+  __syncthreads();
 }
 
 // index i with sl_start[i] <= p < sl_start[i+1], searched in [lo, hi]
@@ -466,10 +492,11 @@ __device__ __forceinline__ void coherent_chunk(const Smem& sm, int flags, int N,
         const double w = sm.wE[i];
         if (w == 0.0) continue;
         const int num = sm.sl_j[i] - b * m2;
-        if (num < 0 || num % a) continue;
-        const int m1 = num / a;
+        if (num < 0) continue;
+        if (a > 1 && num % a) continue;                 // equal rates (a = b = 1): no division
+        const int m1 = (a == 1) ? num : num / a;
         if (m1 >= N) continue;
-        const int idx = sm.sl_start[i] + (m1 - sm.sl_first[i]) / b;
+        const int idx = sm.sl_start[i] + ((b == 1) ? m1 - sm.sl_first[i] : (m1 - sm.sl_first[i]) / b);
         if (m1 < sm.sl_first[i] || idx < p0 || idx >= p_end) continue;
         ISRS_BOUND(idx - p0, CP);
         const double2 y = sm.ybuf[idx - p0];
@@ -487,10 +514,11 @@ __device__ __forceinline__ void coherent_chunk(const Smem& sm, int flags, int N,
         const double w = sm.wF[i];
         if (w == 0.0) continue;
         const int num = sm.sl_j[i] - a * m1;
-        if (num < 0 || num % b) continue;
-        const int m2 = num / b;
+        if (num < 0) continue;
+        if (b > 1 && num % b) continue;
+        const int m2 = (b == 1) ? num : num / b;
         if (m2 >= N || m1 < sm.sl_first[i]) continue;
-        const int idx = sm.sl_start[i] + (m1 - sm.sl_first[i]) / b;
+        const int idx = sm.sl_start[i] + ((b == 1) ? m1 - sm.sl_first[i] : (m1 - sm.sl_first[i]) / b);
         if (idx < p0 || idx >= p_end) continue;
         ISRS_BOUND(idx - p0, CP);
         const double2 y = sm.ybuf[idx - p0];
@@ -1111,28 +1139,40 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
       p0 = p_end;
       i_first = (sm.sl_start[i_last + 1] <= p_end) ? i_last + 1 : i_last;
     }
-    if (COH && (flags & (NEED_G | NEED_H)) && tid == 0) {
-      for (int i = 0; i < S; ++i) {
+    if (COH && (flags & (NEED_G | NEED_H))) {     // block-uniform
+      // G and H of this line segment: lines i = tid, tid + BLOCK, ... per thread, then a fixed-order
+      // block sum (Eqs. 20-21 with C7: G = sum_lines t |line sum|^2, H = |sum_lines t line sum|^2)
+      double v[3] = {0.0, 0.0, 0.0};
+      for (int i = tid; i < S; i += BLOCK) {
         const double2 av = sm.lineacc[i];
-        Ghat = fma(sm.wD[i], fma(av.x, av.x, av.y * av.y), Ghat);
-        hsum.x = fma(sm.wE[i], av.x, hsum.x);
-        hsum.y = fma(sm.wE[i], av.y, hsum.y);
+        v[0] = fma(sm.wD[i], fma(av.x, av.x, av.y * av.y), v[0]);
+        v[1] = fma(sm.wE[i], av.x, v[1]);
+        v[2] = fma(sm.wE[i], av.y, v[2]);
       }
+      block_sum_n<3>(v, sm.red);
+      Ghat += v[0];
+      hsum.x += v[1];
+      hsum.y += v[2];
     }
     __syncthreads();
   }
 
   PROF_MARK(5)   // D / coherent accumulation, chunk tails
-  const double Dsum = block_sum(Dacc, sm.red);
+  // D, and the E / F row and column sums of squares (Eqs. 18-19, C7), by fixed-order block sums
+  double tot[3] = {Dacc, 0.0, 0.0};
+  if (COH) {
+    for (int m = tid; m < N; m += BLOCK) {
+      if (flags & NEED_E) tot[1] = fma(sm.rowacc[m].x, sm.rowacc[m].x, fma(sm.rowacc[m].y, sm.rowacc[m].y, tot[1]));
+      if (flags & NEED_F) tot[2] = fma(sm.colacc[m].x, sm.colacc[m].x, fma(sm.colacc[m].y, sm.colacc[m].y, tot[2]));
+    }
+    block_sum_n<3>(tot, sm.red);
+  } else {
+    tot[0] = block_sum(Dacc, sm.red);
+  }
+  const double Dsum = tot[0];
   if (tid == 0) {
     double* out = p.partials + (size_t)rid * 6;
-    double E = 0.0, F = 0.0;
-    if (COH) {
-      if (flags & NEED_E)
-        for (int m = 0; m < N; ++m) E = fma(sm.rowacc[m].x, sm.rowacc[m].x, fma(sm.rowacc[m].y, sm.rowacc[m].y, E));
-      if (flags & NEED_F)
-        for (int m = 0; m < N; ++m) F = fma(sm.colacc[m].x, sm.colacc[m].x, fma(sm.colacc[m].y, sm.colacc[m].y, F));
-    }
+    const double E = tot[1], F = tot[2];
     out[0] = Dsum * d1 * d2;                                         // D_w
     out[1] = (COH && (flags & NEED_E)) ? E * d1 * d1 * d2 : 0.0;     // E_w
     out[2] = (COH && (flags & NEED_F)) ? F * d2 * d2 * d1 : 0.0;     // F_w
