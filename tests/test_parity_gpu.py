@@ -312,6 +312,13 @@ FULL = {
 
 @pytest.mark.parametrize("cfg", sorted(FULL))
 def test_full_size_region_parity(isrs, cfg):
+    """Sampled per-region partial integrals at full size, written by the very nli() launch bench.py
+    times, against egn.region_partials (the literal oracle) one region at a time.  Whole-eta parity
+    at 1e-10 on every config is test_whole_eta_full_size_matches_golden; this test pins the per-region
+    terms.  Tolerance per term: max(1e-10, 4 eps Theta_max) relative (reading R1: a region whose
+    accumulated dispersion phase reaches Theta_max = max sum_s |chi_s| L_s is determined only to
+    ~eps Theta_max -- the literal oracle forms theta in radians -- so no fp64 evaluation agrees better
+    there), no absolute escape.  The observed errors are printed (pytest -s)."""
     link = bj_config(cfg)
     coi, regs = FULL[cfg]
     with isrs.Engine(link) as e:
@@ -322,17 +329,25 @@ def test_full_size_region_parity(isrs, cfg):
         got = e.region_partials(regs)
         pts, pspans, nreg = e.work()
     assert pspans == pts * link.n_span and nreg > 0
+    worst = 0.0
     for (kappa, k1, k2), g in zip(regs, got):
         want, npts = egn.region_partials(link, kappa, k1, k2)
         if npts == 0:      # empty region: either not listed (-1) or listed with no support
             assert g[5] in (0, -1) and np.all(g[:5] == 0.0) and np.all(want == 0.0)
             continue
         assert g[5] == npts, (cfg, kappa, k1, k2)
-        tol = max(TOL_ETA, 64 * EPS * theta_max(link, kappa, k1, k2))
-        scale = max(np.max(np.abs(want)), 1e-300)
+        th = theta_max(link, kappa, k1, k2)
+        tol = max(TOL_ETA, 4 * EPS * th)
+        rel = [abs(g[t] - want[t]) / abs(want[t]) if want[t] != 0.0 else abs(g[t]) for t in range(5)]
+        print(f"{cfg} region {(kappa, k1, k2)}: Theta_max {th:.3g} rad, tol {tol:.2g}, "
+              f"rel err D..H {['%.1e' % r for r in rel]}")
+        worst = max(worst, max(rel) / tol)
         for t in range(5):
-            assert abs(g[t] - want[t]) <= tol * max(abs(want[t]), 1e-300) or \
-                abs(g[t] - want[t]) <= 1e-13 * scale, (cfg, (kappa, k1, k2), t, g[t], want[t], tol)
+            if want[t] == 0.0:
+                assert g[t] == 0.0, (cfg, (kappa, k1, k2), t, g[t])
+            else:
+                assert rel[t] <= tol, (cfg, (kappa, k1, k2), t, g[t], want[t], tol)
+    print(f"{cfg}: worst error / tolerance {worst:.3g}")
 
 
 @pytest.mark.parametrize("cfg,coi", [("c2", [0, 19, 39]), ("c5", [100])])
