@@ -1158,14 +1158,20 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
   }
 
   PROF_MARK(5)   // D / coherent accumulation, chunk tails
-  // D, and the E / F row and column sums of squares (Eqs. 18-19, C7), by fixed-order block sums
+  // D by the fixed smem tree in both kernels (so the D term of a region is bitwise the same whether
+  // or not its E/F/G/H are needed, pin P12), the E / F row and column sums of squares (Eqs. 18-19,
+  // C7) by fixed-order warp-shuffle block sums
   double tot[3] = {Dacc, 0.0, 0.0};
   if (COH) {
+    tot[0] = block_sum(Dacc, sm.red);
+    double ef[2] = {0.0, 0.0};
     for (int m = tid; m < N; m += BLOCK) {
-      if (flags & NEED_E) tot[1] = fma(sm.rowacc[m].x, sm.rowacc[m].x, fma(sm.rowacc[m].y, sm.rowacc[m].y, tot[1]));
-      if (flags & NEED_F) tot[2] = fma(sm.colacc[m].x, sm.colacc[m].x, fma(sm.colacc[m].y, sm.colacc[m].y, tot[2]));
+      if (flags & NEED_E) ef[0] = fma(sm.rowacc[m].x, sm.rowacc[m].x, fma(sm.rowacc[m].y, sm.rowacc[m].y, ef[0]));
+      if (flags & NEED_F) ef[1] = fma(sm.colacc[m].x, sm.colacc[m].x, fma(sm.colacc[m].y, sm.colacc[m].y, ef[1]));
     }
-    block_sum_n<3>(tot, sm.red);
+    block_sum_n<2>(ef, sm.red);
+    tot[1] = ef[0];
+    tot[2] = ef[1];
   } else {
     tot[0] = block_sum(Dacc, sm.red);
   }
