@@ -43,15 +43,18 @@ def main():
             kms, kps = e.last_kernel_ms()
             pts, pspans, nreg = e.work()
             chain_g, k_s = e.span_chains()
+            grp = e.chain_groups() if a.precision == 64 else None
         eta = eta.cpu().numpy()
-        fl, sl = algorithmic_work_per_point(chain_g, k_s)
+        fl, sl = algorithmic_work_per_point(chain_g, k_s, grp)
         ach = kps[2] * fl / link.n_span / (kms[3] * 1e-3) / 1e12
         print(json.dumps({
             "config": cfg, "n_ch": link.n_ch, "n_span": link.n_span, "grid_n": link.grid_n,
             "precision": a.precision, "regions": nreg, "points": pts, "point_spans": pspans,
             "ms": ms, "kernel_ms": kms, "point_spans_per_s": pspans / (ms * 1e-3),
             "channels_per_s": link.n_ch / (ms * 1e-3), "create_s": t_create,
-            "fp64_flops_frac": ach / fp64_peak_tflops(), "span_chains": [int(g) for g in chain_g],
+            "fp64_flops_frac": ach / fp64_peak_tflops() / (2.0 if a.precision == 32 else 1.0),
+            "span_chains": [int(g) for g in chain_g],
+            "chain_groups": None if grp is None else [int(g) for g in grp],
             "eta_db_min_max": [float(10 * np.log10(eta.min())), float(10 * np.log10(eta.max()))],
             "finite": bool(np.all(np.isfinite(eta)) and np.all(eta > 0))}), flush=True)
 
