@@ -58,6 +58,27 @@ TINY = {
 }
 
 
+def two_chain_groups_link():
+    """Two runs of identical spans, each longer than one 800-segment chain: 12 x 80 km (chains of 10 + 2)
+    then 14 x 60 km (13 + 1), so MODE_SEGGRP has two groups of two chains each (R13)."""
+    link = tiny_link(n_ch=3, rates_gbd=(64,), n_span=26, grid_n=8, fmts=("16qam", "qpsk"))
+    L = np.r_[np.full(12, 80e3), np.full(14, 60e3)]
+    return link.with_(length_m=L)
+
+
+def test_eta_parity_two_chain_groups(isrs):
+    link = two_chain_groups_link()
+    with isrs.Engine(link) as e:
+        g = e.chain_groups()
+        chains, _ = e.span_chains()
+    assert list(chains) == [10, 2, 13, 1] and list(g) == [0, 2, 4]
+    e_o, t_o = egn.eta(link)
+    e_g, t_g = gpu_eta(isrs, link)
+    assert np.all(np.abs(e_g - e_o) / e_o <= TOL_ETA), np.abs(e_g - e_o) / e_o
+    scale = np.abs(t_o).sum(axis=1, keepdims=True)
+    assert np.all(np.abs(t_g - t_o) <= TOL_ETA * scale)
+
+
 @pytest.mark.parametrize("name", sorted(TINY))
 def test_eta_parity_tiny(isrs, name):
     link = tiny_link(**TINY[name])

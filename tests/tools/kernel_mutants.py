@@ -38,11 +38,30 @@ MUTANTS = {
     "lattice_m2": ("kernels.cu", "const int m2f = (b == 1) ? lj - a * m1f : (lj - a * m1f) / b;",
                    "const int m2f = (b == 1) ? lj - a * m1f : (lj - a * m1f) / b + (a > 1);",
                    "point geometry: m2 off by one on mixed-rate lattices"),
+    # ---- round 2: chain groups (R13), shuffle reductions, the exact planner
+    "group_horner_conj": ("kernels.cu", "const double t = fma(sr[q], a, fma(-si[q], b, accr[q]));",
+                          "const double t = fma(sr[q], a, fma(si[q], b, accr[q]));",
+                          "chain groups: Horner step with conj(w) in the real part"),
+    "group_step_short": ("kernels.cu", "const double t = x * (double)(Ks * G0);",
+                         "const double t = x * (double)(Ks * (G0 - 1));",
+                         "chain groups: w = e^{i (G0 - 1) chi L}"),
+    "group_theta_short": ("kernels.cu", "const double t2 = fma(x, (double)(Ks * gsum), th[q]);",
+                          "const double t2 = fma(x, (double)(Ks * (gsum - 1)), th[q]);",
+                          "chain groups: theta advanced by one span too few per group"),
+    "group_second_phase": ("kernels.cu", "if (gr > 0) sincospi_d(th[q], &ps, &pc);",
+                           "if (gr > 1) sincospi_d(th[q], &ps, &pc);",
+                           "chain groups: the second group's span phase dropped"),
+    "shuffle_last_warp": ("kernels.cu", "for (int w = 1; w < BLOCK / 32; ++w) t += red[NV * w + k];",
+                          "for (int w = 1; w < BLOCK / 32 - 1; ++w) t += red[NV * w + k];",
+                          "coherent block sums: the last warp's partial dropped"),
+    "planner_touching_twice": ("abi.cu", "if (j0 <= cur1) {                         // touching bands share the edge line",
+                               "if (j0 < cur1) {                         // touching bands share the edge line",
+                               "planner: the edge line of touching bands counted twice"),
 }
 
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fvisibility=hidden", "-shared", "--expt-relaxed-constexpr"]
-TESTS = "tiny or edge or random_links or c1_full or streams"
+TESTS = "tiny or edge or random_links or c1_full or streams or planned_work or chain_groups or (golden and c2_eta)"
 
 
 def build():
