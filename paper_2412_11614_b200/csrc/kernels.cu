@@ -900,6 +900,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
           const double2* rowp = (const double2*)(sm.T + (li - tb) * p.tstride);
           // thread-private smem slots (column tid: conflict-free) hold what is only needed between
           // chains, so the recurrence runs with the register budget of a single chain
+          ISRS_BOUND((5 * PPT - 1) * BLOCK + tid, 5 * PPT * BLOCK);
           double* gu = sm.gst + tid;                        // [q * BLOCK]: (f1 - f)(f2 - f)
           double* gs = sm.gst + PPT * BLOCK + tid;          // f1 + f2
           double* gx = sm.gst + 2 * PPT * BLOCK + tid;      // chi h / pi
