@@ -972,8 +972,14 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
           // chain of G identical consecutive spans starting at s (G = 1 unless chained, R9)
           const int s = __ldg(p.chain_s0 + ch), G = __ldg(p.chain_g + ch);
           const int cls = __ldg(p.cls + s);
+#ifdef ISRS_DIAG_NO_REBUILD
+          // diagnostic builds only (wrong values): keep the first span's table for every span, to bound
+          // what the per-span table costs on multi-class links
+          if ((SEGM || MODE == MODE_SEG32) && (tcls < 0 || i_first < tb || i_last >= tb + tn)) {
+#else
           if ((SEGM || MODE == MODE_SEG32) &&
               (cls != tcls || i_first < tb || i_last >= tb + tn)) {
+#endif
             // ---- (re)build the envelope table rows for compacted lines [tb, tb + tn)
             __syncthreads();
             tb = i_first;
