@@ -87,9 +87,11 @@ def ncu_traffic(config="c5"):
     `ncu --set full` summary of `config` under profiles/ (tools/ncu_summary.py), or (None, None)."""
     import glob
     best = None
-    def order(fn):            # r01a < ... < r01z < r01aa < r01ab: by tag length, then name
+    def order(fn):            # r01a < ... < r01z < r01aa < ... < r02a < ...: by round, suffix length, suffix
+        import re
         tag = os.path.basename(fn).split("_")[0]
-        return (len(tag), tag)
+        m = re.match(r"r(\d+)([a-z]+)$", tag)
+        return (int(m.group(1)), len(m.group(2)), m.group(2)) if m else (0, len(tag), tag)
 
     for fn in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_integrand*.json")), key=order):
         if "fp32" in fn or f"_{config}" not in fn:   # the bench config's capture only

@@ -64,9 +64,14 @@ def test_traffic_source_is_the_newest_capture_of_the_config(cfg):
     import glob
     import bench
     traffic, src = bench.ncu_traffic(cfg)
+    import re
     caps = [os.path.basename(f).split("_")[0] for f in glob.glob(os.path.join(ROOT, "profiles", f"*ncu_integrand*_{cfg}*.json"))
             if "fp32" not in f]
-    newest = max(caps, key=lambda t: (len(t), t))
+
+    def key(t):
+        m = re.match(r"r(\d+)([a-z]+)$", t)
+        return (int(m.group(1)), len(m.group(2)), m.group(2))
+    newest = max(caps, key=key)
     assert src is not None and os.path.basename(src).startswith(newest + "_") and traffic > 0
 
 
