@@ -473,6 +473,20 @@ def run_ours(args, link, coi, ws, rank, local):
                  "note": "ISRS_EGN_FLAG_DEDUP: one K-segment sum per run of identical spans x the "
                          "phased-array factor; same eta (<= 1e-10), not the headline"}
 
+    # f1 <-> f2 symmetry (ISRS_EGN_FLAG_MIRROR), reported separately like dedup: region (k, k1, k2),
+    # k1 < k2, evaluated once for both orientations; rate in LOGICAL point-spans/s
+    mirror = None
+    if ws == 1 and not args.no_dedup:
+        with isrs.Engine(link, device=local, precision=args.precision, flags=isrs.FLAG_MIRROR) as em:
+            mms, _, _ = time_steps(em, lambda: em.nli_into(eta.data_ptr(), 0, coi, stream.cuda_stream),
+                                   stream, flush, 3, 2)
+            mpts = em.work()[0]
+        mm = float(np.median(mms))
+        mirror = {"value": pspans / (mm * 1e-3), "unit": UNIT + " (logical)", "ms_per_step": mm,
+                  "evaluated_point_spans_per_step": mpts * link.n_span,
+                  "note": "ISRS_EGN_FLAG_MIRROR: f1 <-> f2 symmetry (pin P2), each off-diagonal region pair "
+                          "evaluated once; same eta (<= 1e-12 of the full evaluation), not the headline"}
+
     extras = {}
     if ws == 1 and not args.no_extra:
         for name, spec in (("c2", "all"), ("c4", "default")):
@@ -524,6 +538,8 @@ def run_ours(args, link, coi, ws, rank, local):
             line["eta_bitwise_equal_across_ranks"] = same_eta
         if dedup is not None:
             line["dedup_effective"] = dedup
+        if mirror is not None:
+            line["mirror_effective"] = mirror
         if extras:
             line["other_configs"] = extras
         if not args.no_cpu and ws == 1:

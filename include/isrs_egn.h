@@ -101,11 +101,17 @@ enum { ISRS_EGN_FLAG_UNIT_LINK = 1u, /* test hook: Y := 1 (oracle pin P6)       
                                         and multiply by the phased-array factor sum_g e^{i g chi L};
                                         same Y (Eq. 22), ~G x less work.  Its rate is reported
                                         separately, never as the headline point-spans/s */
-       ISRS_EGN_FLAG_LITERAL_GAIN = 8u /* NEXT-4b (R11): Eq. 22's gain / sqrt(rho) products
+       ISRS_EGN_FLAG_LITERAL_GAIN = 8u, /* NEXT-4b (R11): Eq. 22's gain / sqrt(rho) products
                                         as printed with a transparent scalar gain g_s = e^{alpha_s L_s}
                                         (mean loss restored, SRS tilt persists) instead of reading C3's
                                         ideal per-frequency equalisation (products = 1); fp64 segment
-                                        mode only */ };
+                                        mode only */
+       ISRS_EGN_FLAG_MIRROR = 16u    /* f1 <-> f2 symmetry (Eqs. 5, 8, 22 and the gates are symmetric in
+                                        f1, f2; pin P2): region (kappa, k1, k2), k1 < k2, is evaluated once
+                                        and also yields (kappa, k2, k1) with E and F exchanged -- about half
+                                        the point-spans evaluated, the same eta.  Like DEDUP its rate is
+                                        reported separately (logical point-spans), never as the headline.
+                                        Not with isrs_egn_nli_shard (EUNSUPPORTED). */ };
 
 typedef struct {
   int32_t grid_n;      /* N: N x N bin-centre grid per (kappa1, kappa2) region; even, >= 2 (C6) */

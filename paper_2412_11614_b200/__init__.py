@@ -13,11 +13,11 @@ import ctypes
 import numpy as np
 
 from . import _abi
-from ._abi import (FLAG_DEDUP, FLAG_LITERAL_GAIN, FLAG_NO_CHAIN, FLAG_UNIT_LINK, MU_INTEGRAL, MU_MACLAURIN, MU_SEGMENT,
+from ._abi import (FLAG_DEDUP, FLAG_LITERAL_GAIN, FLAG_MIRROR, FLAG_NO_CHAIN, FLAG_UNIT_LINK, MU_INTEGRAL, MU_MACLAURIN, MU_SEGMENT,
                    IsrsEgnError, ProblemArrays,  # noqa: F401
                    numerics)
 
-__all__ = ["Engine", "NliGraph", "eta_host", "plan_shards", "IsrsEgnError", "MU_SEGMENT", "MU_MACLAURIN", "MU_INTEGRAL", "FLAG_UNIT_LINK", "FLAG_NO_CHAIN", "FLAG_DEDUP", "FLAG_LITERAL_GAIN",
+__all__ = ["Engine", "NliGraph", "eta_host", "plan_shards", "IsrsEgnError", "MU_SEGMENT", "MU_MACLAURIN", "MU_INTEGRAL", "FLAG_UNIT_LINK", "FLAG_NO_CHAIN", "FLAG_DEDUP", "FLAG_LITERAL_GAIN", "FLAG_MIRROR",
            "library_path"]
 
 

@@ -18,6 +18,7 @@ FLAG_UNIT_LINK = 1
 FLAG_NO_CHAIN = 2
 FLAG_DEDUP = 4
 FLAG_LITERAL_GAIN = 8
+FLAG_MIRROR = 16
 
 EXPORTED = ("isrs_egn_create", "isrs_egn_nli", "isrs_egn_region_partials", "isrs_egn_work", "isrs_egn_last_work",
             "isrs_egn_eta_host", "isrs_egn_last_kernel_ms", "isrs_egn_last_launch_count",

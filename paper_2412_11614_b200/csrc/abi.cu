@@ -168,6 +168,7 @@ struct WorkList {
   std::vector<int> coi;
   std::vector<double> fv;   // NLI frequency of each (COI, f sample)
   std::vector<RegionDesc> desc;
+  std::vector<int> mirror;   // ISRS_EGN_FLAG_MIRROR: id of (kappa, k2, k1) written by region id, or -1
   std::vector<long long> coi_off;
   std::vector<int> list_d, list_c;
 };
@@ -199,7 +200,7 @@ struct isrs_egn {
   bool have_wl = false;
   DevBuf<RegionDesc> d_desc;
   DevBuf<long long> d_coi_off;
-  DevBuf<int> d_coi, d_list_d, d_list_c;
+  DevBuf<int> d_coi, d_list_d, d_list_c, d_mirror;
   DevBuf<double> d_fv;
   // regions launched by the last call (the whole list, or one shard of it)
   std::vector<int> act_d, act_c;
@@ -636,9 +637,12 @@ static void build_worklist(const isrs_egn* h, const std::vector<int>& coi, WorkL
   w->coi_off.assign(1, 0);
   w->list_d.clear();
   w->list_c.clear();
+  w->mirror.clear();
   std::vector<long long>& cost = w->cost;
   cost.clear();
   const int nc = h->n_ch;
+  const bool mirror = (h->num.flags & ISRS_EGN_FLAG_MIRROR) != 0;
+  std::vector<int> idmap;
   const int fs = h->num.f_samples, nfs = std::max(1, fs);
   for (int kappa : coi) {
    for (int m = 0; m < nfs; ++m) {
@@ -647,6 +651,8 @@ static void build_worklist(const isrs_egn* h, const std::vector<int>& coi, WorkL
                                : h->lo[kappa] + (2.0 * m + 1.0) * (h->R[kappa] / (2.0 * fs));
     const int fvi = (int)w->fv.size();
     w->fv.push_back(f);
+    const size_t first = w->desc.size();
+    if (mirror) idmap.assign((size_t)nc * nc, -1);
     for (int k1 = 0; k1 < nc; ++k1) {
       for (int k2 = 0; k2 < nc; ++k2) {
         const double lo3 = h->lo[k1] + h->lo[k2] - f + (h->delta[k1] + h->delta[k2]) / 2;
@@ -662,8 +668,23 @@ static void build_worklist(const isrs_egn* h, const std::vector<int>& coi, WorkL
         if (h->psi[k1] != 0.0 && k1 == k2 && overlaps(k1)) flags |= NEED_H;
         const int id = (int)w->desc.size();
         w->desc.push_back(RegionDesc{kappa, k1, k2, flags | (fvi << FV_SHIFT)});
-        (flags ? w->list_c : w->list_d).push_back(id);
         cost.push_back(region_points(h, f, k1, k2));
+        if (mirror) {
+          idmap[(size_t)k1 * nc + k2] = id;
+          w->mirror.push_back(-1);
+        } else {
+          (flags ? w->list_c : w->list_d).push_back(id);
+        }
+      }
+    }
+    if (mirror) {
+      // f1 <-> f2 symmetry: region (kappa, k1, k2), k1 < k2, also yields (kappa, k2, k1) (the region
+      // filter is symmetric, so both are listed or neither); diagonal regions are computed as usual
+      for (size_t id = first; id < w->desc.size(); ++id) {
+        const RegionDesc& rd = w->desc[id];
+        if (rd.k1 > rd.k2) continue;
+        if (rd.k1 < rd.k2) w->mirror[id] = idmap[(size_t)rd.k2 * nc + rd.k1];
+        ((rd.flags & (NEED_E | NEED_F | NEED_G | NEED_H)) ? w->list_c : w->list_d).push_back((int)id);
       }
     }
    }
@@ -772,6 +793,8 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
     DevBuf<long long> coi_off;
     DevBuf<int> coi_d, list_d, list_c;
     DevBuf<double> fv, partials, npts;
+    DevBuf<int> mir;
+    if (!wl.mirror.empty()) pk.add(&mir, wl.mirror);
     pk.add(&desc, wl.desc); pk.add(&coi_off, wl.coi_off); pk.add(&coi_d, wl.coi);
     pk.add(&list_d, wl.list_d); pk.add(&list_c, wl.list_c); pk.add(&fv, wl.fv);
     pk.reserve(&partials, wl.desc.size() * 6);
@@ -780,6 +803,7 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
     if (ce != cudaSuccess) return fail(ISRS_EGN_ENOMEM, std::string("work-list allocation failed: ") + cudaGetErrorString(ce));
     h->d_desc = desc; h->d_coi_off = coi_off; h->d_coi = coi_d; h->d_list_d = list_d;
     h->d_list_c = list_c; h->d_fv = fv; h->d_partials = partials; h->d_npts = npts;
+    h->d_mirror = mir;
     h->wl = std::move(wl);
     h->have_wl = true;
     h->sh_rank = h->sh_world = -1;
@@ -838,6 +862,7 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
   kp.lnA = h->d_lnA.p; kp.zeta = h->d_zeta.p; kp.Kc = h->d_Kc.p; kp.n_cls = h->n_cls;
   kp.kstride = h->kstride; kp.tstride = h->tstride; kp.tw = h->tw; kp.N = h->N;
   kp.fv = h->d_fv.p; kp.desc = h->d_desc.p; kp.partials = h->d_partials.p;
+  kp.mirror = (h->num.flags & ISRS_EGN_FLAG_MIRROR) ? h->d_mirror.p : nullptr;
   kp.mode = mode;
   int launches = 0;
 #ifdef ISRS_PROF
@@ -912,6 +937,8 @@ extern "C" int isrs_egn_nli_shard(isrs_egn_t* h, int32_t n_coi, const int32_t* c
   if (!coi_sums_dev) return fail(ISRS_EGN_EINVAL, "coi_sums_dev is NULL");
   NvtxRange nv("isrs_egn_nli_shard");
   if (world < 1 || rank < 0 || rank >= world) return fail(ISRS_EGN_EINVAL, "rank/world out of range");
+  if (h->num.flags & ISRS_EGN_FLAG_MIRROR)
+    return fail(ISRS_EGN_EUNSUPPORTED, "FLAG_MIRROR writes partner regions across the region list: no shards");
   std::vector<int> c;
   int rc = coi_list(h, n_coi, coi, &c);
   if (rc) return rc;

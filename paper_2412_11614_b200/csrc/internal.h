@@ -143,6 +143,8 @@ struct KParams {
   const double* fv;     // NLI frequencies (offsets) indexed by flags >> FV_SHIFT
   const RegionDesc* desc;
   double* partials;     // [n_regions][6]: D_w, E_w, F_w, G_w, H_w, n_points
+  const int* mirror;    // ISRS_EGN_FLAG_MIRROR: [n_regions] canonical id of region (kappa, k2, k1) whose
+                        // partials this region's launch also writes (E and F swapped), or -1; NULL = off
   int mode;
   unsigned long long* prof;   // ISRS_PROF builds only: per-phase warp-cycle counters [8]
 };

@@ -1192,6 +1192,21 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
     out[3] = (COH && (flags & NEED_G)) ? Ghat * d1 * d1 * d1 : 0.0;  // G_w (k1 == k2)
     out[4] = (COH && (flags & NEED_H)) ? (hsum.x * hsum.x + hsum.y * hsum.y) * (d1 * d2) * (d1 * d2) : 0.0;
     out[5] = (double)npts_total;
+    if (p.mirror) {
+      // f1 <-> f2 symmetry (Eqs. 5, 8, 22 are symmetric in f1, f2; pin P2): region (kappa, k2, k1) has
+      // the same Y at the mirrored points, hence the same D_w and n_points, with E and F exchanged
+      // (its coherent-over-f1 sum is this region's coherent-over-f2 sum); G and H need k1 == k2
+      const int mr = __ldg(p.mirror + rid);
+      if (mr >= 0) {
+        double* o2 = p.partials + (size_t)mr * 6;
+        o2[0] = out[0];
+        o2[1] = out[2];
+        o2[2] = out[1];
+        o2[3] = 0.0;
+        o2[4] = 0.0;
+        o2[5] = out[5];
+      }
+    }
   }
   PROF_MARK(6)   // epilogue (block sum, partials)
   PROF_FLUSH

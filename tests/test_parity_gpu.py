@@ -158,6 +158,8 @@ RANDOM_MODES = {
     "no_chain": ({}, lambda m: {"flags": m.FLAG_NO_CHAIN}, "rel"),
     "fp32": ({}, lambda m: {"precision": 32}, "db"),
     "3d_f2": ({"f_samples": 2}, lambda m: {"f_samples": 2}, "rel"),
+    "mirror": ({}, lambda m: {"flags": m.FLAG_MIRROR}, "rel"),
+    "mirror_3d": ({"f_samples": 2}, lambda m: {"flags": m.FLAG_MIRROR, "f_samples": 2}, "rel"),
 }
 
 
@@ -664,3 +666,38 @@ def test_precompute_tables_match_the_oracle_profile(isrs, cfg):
             assert np.all(np.abs(ze - z_o) <= 1e-14 * np.abs(z_o)), (cfg, s)
             lna_o = np.log(c_o) - sp["alpha"] * h * np.arange(K)
             assert np.all(np.abs(la - lna_o) <= 1e-14 * np.maximum(1.0, np.abs(lna_o))), (cfg, s)
+
+
+@pytest.mark.parametrize("name", sorted(TINY))
+def test_mirror_mode_parity_tiny(isrs, name):
+    """ISRS_EGN_FLAG_MIRROR (f1 <-> f2 symmetry, pin P2): half the off-diagonal regions evaluated, the
+    oracle's eta and D..H to the same bar."""
+    link = tiny_link(**TINY[name])
+    e_o, t_o = egn.eta(link)
+    e_g, t_g = gpu_eta(isrs, link, flags=isrs.FLAG_MIRROR)
+    assert np.all(np.abs(e_g - e_o) / e_o <= TOL_ETA), (name, np.abs(e_g - e_o) / e_o)
+    scale = np.abs(t_o).sum(axis=1, keepdims=True)
+    assert np.all(np.abs(t_g - t_o) <= TOL_ETA * scale), name
+
+
+@pytest.mark.parametrize("cfg,coi", [("c2", None), ("c4", [0, 40, 79]), ("c5", [100])])
+def test_mirror_mode_equals_full_evaluation(isrs, cfg, coi):
+    link = bj_config(cfg)
+    a, ta = gpu_eta(isrs, link, coi=coi, flags=isrs.FLAG_MIRROR)
+    b, tb = gpu_eta(isrs, link, coi=coi)
+    assert np.all(np.abs(a - b) / b <= 1e-12), np.abs(a - b) / b
+    assert np.all(np.abs(ta - tb) <= 1e-12 * np.abs(tb).sum(axis=1, keepdims=True))
+    with isrs.Engine(link, flags=isrs.FLAG_MIRROR) as e:
+        e.nli(coi=coi)
+        pts_eval = e.work()[0]
+        pts_logical = e.planned_work(coi)[0]
+        with pytest.raises(isrs.IsrsEgnError):
+            e.nli_shard(0, 2, coi=coi)
+    assert pts_eval < 0.6 * pts_logical          # about half the points evaluated
+
+
+def test_mirror_mode_fp32(isrs):
+    link = tiny_link(**TINY["mixed_rates_guard"])
+    e_o, _ = egn.eta(link)
+    e_g, _ = gpu_eta(isrs, link, precision=32, flags=isrs.FLAG_MIRROR)
+    assert np.all(np.abs(10 * np.log10(e_g / e_o)) <= 1e-3)
