@@ -203,7 +203,9 @@ struct isrs_egn {
   DevBuf<int> d_coi, d_list_d, d_list_c, d_mirror;
   DevBuf<double> d_fv;
   // regions launched by the last call (the whole list, or one shard of it)
-  std::vector<int> act_d, act_c;
+  // regions launched by the last call: the work list's own launch lists, or the current shard's
+  const std::vector<int>* act_d = nullptr;
+  const std::vector<int>* act_c = nullptr;
   std::vector<int> sh_act_d, sh_act_c;   // the regions of the current shard (rank, world)
   int sh_rank = -1, sh_world = -1;
   long long sh_lo = 0, sh_hi = 0;
@@ -806,6 +808,7 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
     h->d_mirror = mir;
     h->wl = std::move(wl);
     h->have_wl = true;
+    h->have_result = false;   // the new partials hold nothing until this call's kernels ran
     h->sh_rank = h->sh_world = -1;
   }
   const int* dl_d = h->d_list_d.p;
@@ -835,15 +838,15 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
       h->sh_act_d = std::move(act_d);
       h->sh_act_c = std::move(act_c);
     }
-    h->act_d = h->sh_act_d;
-    h->act_c = h->sh_act_c;
+    h->act_d = &h->sh_act_d;
+    h->act_c = &h->sh_act_c;
     dl_d = h->d_sh_d.p;
     dl_c = h->d_sh_c.p;
     r_lo = h->sh_lo;
     r_hi = h->sh_hi;
   } else {
-    h->act_d = h->wl.list_d;
-    h->act_c = h->wl.list_c;
+    h->act_d = &h->wl.list_d;
+    h->act_c = &h->wl.list_c;
   }
   KParams kp{};
   kp.lo = h->d_lo.p; kp.hi = h->d_hi.p; kp.f = h->d_f.p; kp.G = h->d_G.p; kp.R = h->d_R.p;
@@ -878,11 +881,11 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
   cudaEventRecord(fork, st);
   cudaStreamWaitEvent(h->side, fork, 0);
   if (!capturing) cudaEventRecord(h->evc[0], h->side);
-  if (launch_integrand(kp, dl_c, (long long)h->act_c.size(), true, h->side, &launches) != 0)
+  if (launch_integrand(kp, dl_c, (long long)h->act_c->size(), true, h->side, &launches) != 0)
     return cuda_fail(cudaGetLastError(), "integrand launch (coherent regions)");
   if (!capturing) cudaEventRecord(h->evc[1], h->side);
   cudaEventRecord(join, h->side);
-  if (launch_integrand(kp, dl_d, (long long)h->act_d.size(), false, st, &launches) != 0)
+  if (launch_integrand(kp, dl_d, (long long)h->act_d->size(), false, st, &launches) != 0)
     return cuda_fail(cudaGetLastError(), "integrand launch (D-only regions)");
   if (!capturing) cudaEventRecord(h->ev[1], st);
   cudaStreamWaitEvent(st, join, 0);
@@ -895,8 +898,8 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
   launches += 1;
   if (capturing) return ISRS_EGN_OK;     // the handle's timing / ordering state describes direct calls
   cudaEventRecord(h->ev[3], st);
-  h->launched[0] = !h->act_d.empty();
-  h->launched[1] = !h->act_c.empty();
+  h->launched[0] = !h->act_d->empty();
+  h->launched[1] = !h->act_c->empty();
 #ifdef ISRS_PROF
   {
     unsigned long long hp[16];
@@ -1046,11 +1049,11 @@ extern "C" int isrs_egn_last_work(isrs_egn_t* h, int64_t* points, int64_t* point
                     cudaMemcpyDeviceToHost);
   if (ce != cudaSuccess) return cuda_fail(ce, "npts copy");
   long long tot = 0;
-  for (int id : h->act_d) tot += (long long)np[id];
-  for (int id : h->act_c) tot += (long long)np[id];
+  for (int id : *h->act_d) tot += (long long)np[id];
+  for (int id : *h->act_c) tot += (long long)np[id];
   if (points) *points = tot;
   if (point_spans) *point_spans = tot * h->n_span;
-  if (regions) *regions = (long long)(h->act_d.size() + h->act_c.size());
+  if (regions) *regions = (long long)(h->act_d->size() + h->act_c->size());
   return ISRS_EGN_OK;
 }
 
@@ -1078,8 +1081,8 @@ extern "C" int isrs_egn_last_kernel_ms(isrs_egn_t* h, double* ms_out, double* po
                       sizeof(double), nr, cudaMemcpyDeviceToHost);
     if (ce != cudaSuccess) return cuda_fail(ce, "npts copy");
     double a = 0, b = 0;
-    for (int id : h->act_d) a += np[id];
-    for (int id : h->act_c) b += np[id];
+    for (int id : *h->act_d) a += np[id];
+    for (int id : *h->act_c) b += np[id];
     point_spans_out[0] = a * h->n_span;
     point_spans_out[1] = b * h->n_span;
     point_spans_out[2] = (a + b) * h->n_span;
