@@ -213,7 +213,8 @@ struct isrs_egn {
   DevBuf<double> d_partials, d_npts;
   Arena arena_create, arena_plan, arena_shard;
   cudaStream_t last_stream = nullptr;
-  bool have_result = false;
+  bool have_result = false;   // the partials hold the last call's values
+  bool ordered = false;       // ev[3] marks the end of the handle's last direct call (on last_stream)
   int last_launches = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   // coherent-region integrand on a side stream, concurrent with the D-only launch (fills its tail)
@@ -786,7 +787,7 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
     return cuda_fail(cudaGetLastError(), "integrand kernel attributes");
   // calls on one handle share its partials (and a rebuild frees the previous work list): a call on
   // another stream than the previous one waits (on the device) for the previous call's end
-  if (!capturing && h->have_result && st != h->last_stream) cudaStreamWaitEvent(st, h->ev[3], 0);
+  if (!capturing && h->ordered && st != h->last_stream) cudaStreamWaitEvent(st, h->ev[3], 0);
   if (rebuild) {
     WorkList wl;
     build_worklist(h, c, &wl);
@@ -809,6 +810,9 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
     h->wl = std::move(wl);
     h->have_wl = true;
     h->have_result = false;   // the new partials hold nothing until this call's kernels ran
+    cudaEventRecord(h->ev[3], st);   // later calls on other streams order behind this rebuild
+    h->ordered = true;
+    h->last_stream = st;
     h->sh_rank = h->sh_world = -1;
   }
   const int* dl_d = h->d_list_d.p;
@@ -837,6 +841,9 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
       h->sh_world = world;
       h->sh_act_d = std::move(act_d);
       h->sh_act_c = std::move(act_c);
+      cudaEventRecord(h->ev[3], st);   // later calls on other streams order behind this upload
+      h->ordered = true;
+      h->last_stream = st;
     }
     h->act_d = &h->sh_act_d;
     h->act_c = &h->sh_act_c;
@@ -898,6 +905,7 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
   launches += 1;
   if (capturing) return ISRS_EGN_OK;     // the handle's timing / ordering state describes direct calls
   cudaEventRecord(h->ev[3], st);
+  h->ordered = true;
   h->launched[0] = !h->act_d->empty();
   h->launched[1] = !h->act_c->empty();
 #ifdef ISRS_PROF
