@@ -28,8 +28,9 @@
  * create (synchronous), destroy (synchronises the device) and the inspection calls that say so.
  * Errors: every call returns a status and isrs_egn_last_error() (thread-local) names the offending
  * field / index.  Validation, work-list limits, allocation and kernel attributes are checked before
- * the first kernel is enqueued, so on those errors nothing is enqueued and outputs are untouched; a
- * CUDA launch failure after that point (ECUDA) may leave a partial enqueue whose outputs are undefined.
+ * the first kernel is enqueued, so on those errors no kernel runs and outputs are untouched (a work
+ * list already rebuilt for the new COI set stays valid for the next call); a CUDA launch failure after
+ * that point (ECUDA) may leave a partial enqueue whose outputs are undefined.
  * CUDA graphs: once a handle has run a COI set (and shard) on a non-capturing stream, a further call
  * for the same set neither allocates nor synchronises, so it can be captured (cudaStreamBeginCapture)
  * and replayed; inside a capture the call records no timing or ordering events and leaves
