@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libisrs_egn.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("abi.cu", "kernels.cu")]
-HEADERS = [os.path.join(HERE, "csrc", "internal.h"), os.path.join(ROOT, "include", "isrs_egn.h")]
+HEADERS = [os.path.join(HERE, "csrc", "internal.h"), os.path.join(HERE, "csrc", "cis_table.h"), os.path.join(ROOT, "include", "isrs_egn.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-shared",
               "-Xptxas", "-v", "--expt-relaxed-constexpr"]

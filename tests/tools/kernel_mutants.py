@@ -4,6 +4,7 @@ ISRS_EGN_LIB: every mutant must fail them.
 
     python tests/tools/kernel_mutants.py build          # here (nvcc cross-compiles): build_variants/lib_mut_*.so
     python tests/tools/kernel_mutants.py run            # on the GPU box: one pytest run per mutant
+    (either with mutant names after the verb: only those)
 
 Prints one JSON line per mutant: name, slip, pytest exit code, killed (exit code 1).
 """
@@ -57,6 +58,16 @@ MUTANTS = {
     "planner_touching_twice": ("abi.cu", "if (j0 <= cur1) {                         // touching bands share the edge line",
                                "if (j0 < cur1) {                         // touching bands share the edge line",
                                "planner: the edge line of touching bands counted twice"),
+    # ---- round 2, late: the table-driven sin/cos(pi x)
+    "cistab_index": ("kernels.cu", "const double2 e = __ldg(&kCisTab[__double2loint(t) & 255]);",
+                     "const double2 e = __ldg(&kCisTab[(__double2loint(t) + 1) & 255]);",
+                     "table sincospi: the neighbouring table entry"),
+    "cistab_sin_sign": ("kernels.cu", "*sp = fma(e.y, cm1, fma(e.x, s, e.y));",
+                        "*sp = fma(e.y, cm1, fma(-e.x, s, e.y));",
+                        "table sincospi: sin(a + b) with -cos(a) sin(b)"),
+    "cistab_cos_term": ("kernels.cu", "pc = fma(pc, r2, -4.934802200544679);",
+                        "pc = fma(pc, r2, -4.934802200544679 * 0.999);",
+                        "table sincospi: the r^2 coefficient of cos off by 0.1 %"),
 }
 
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
@@ -64,9 +75,14 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-Xc
 TESTS = "tiny or edge or random_links or c1_full or streams or planned_work or chain_groups or (golden and c2_eta)"
 
 
+def _selected():
+    names = sys.argv[2:]
+    return {k: v for k, v in MUTANTS.items() if not names or k in names}
+
+
 def build():
     os.makedirs(OUT, exist_ok=True)
-    for name, (fn, old, new, _) in MUTANTS.items():
+    for name, (fn, old, new, _) in _selected().items():
         with tempfile.TemporaryDirectory() as td:
             src = os.path.join(td, "paper_2412_11614_b200", "csrc")
             shutil.copytree(os.path.join(ROOT, "paper_2412_11614_b200", "csrc"), src)
@@ -83,7 +99,7 @@ def build():
 
 
 def run():
-    for name, (_, _, _, what) in MUTANTS.items():
+    for name, (_, _, _, what) in _selected().items():
         lib = os.path.join(OUT, f"lib_mut_{name}.so")
         env = dict(os.environ, ISRS_EGN_LIB=lib)
         r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_parity_gpu.py"),
