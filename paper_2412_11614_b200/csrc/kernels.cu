@@ -668,7 +668,6 @@ __device__ __forceinline__ void span_seg32(const KParams& p, int ch, int G, int 
   }
 #pragma unroll
   for (int hq = 0; hq < PPT / 2; ++hq) c2[hq] = make_float2(2.f * cf[2 * hq], 2.f * cf[2 * hq + 1]);
-  const float2 neg1 = make_float2(-1.f, -1.f);
   const int n4 = Kp4 >> 2;
   // the run's Y contribution in fp32 (<= CHAIN_MAX / K spans), added to the fp64 Y once per run
   float ayr[PPT], ayi[PPT];
@@ -687,7 +686,9 @@ __device__ __forceinline__ void span_seg32(const KParams& p, int ch, int G, int 
       for (int hq = 0; hq < PPT / 2; ++hq) {
         // (2cos b_{k+1} + a) - b_{k+2}: the shared a in the addend slot (operand reuse)
         const float2 t = __ffma2_rn(c2[hq], b1[hq], make_float2(a, a));
-        const float2 n = __ffma2_rn(b2[hq], neg1, t);
+        // - b_{k+2} as FADD2 with a negated operand (two register pairs read instead of three; the
+        // same value as FFMA2 by -1: c2 -0.2 %, c5 -0.1 %, profiles/r02zd_variants_fp32_fadd2.txt)
+        const float2 n = __fadd2_rn(t, make_float2(-b2[hq].x, -b2[hq].y));
         b2[hq] = b1[hq];
         b1[hq] = n;
       }
