@@ -1,4 +1,5 @@
 #!/bin/bash
+# (ran a MODE_SEGPF build that is not in the tree: the experiment was reverted, see profiles/r02zb_*)
 # MODE_SEGPF (double-buffered prebuilt table on multi-class links) vs the single-buffer kernel
 OUT=gpurun_out/r02zb; mkdir -p $OUT
 python -m paper_2412_11614_b200.build > $OUT/build.log 2>&1

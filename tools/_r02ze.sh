@@ -1,4 +1,5 @@
 #!/bin/bash
+# (lib_pf32 / lib_pf48 were built from a patched copy of csrc/ with MODE_SEGPF, reverted; see profiles/r02ze_*)
 # c4: double-buffered prebuilt table (MODE_SEGPF) at 32 KB (20 rows per buffer) and 48 KB (30 rows per
 # buffer) table budgets, each against the single-buffer kernel of the same build (ISRS_EGN_NO_SEGPF=1)
 OUT=gpurun_out/r02ze; mkdir -p $OUT

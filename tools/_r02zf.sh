@@ -1,4 +1,5 @@
 #!/bin/bash
+# (lib_step1 was built from a since-reverted tree with precomputed walk steps; see profiles/r02zf_*)
 # precomputed envelope walk steps e^{-zeta_k g} (step1) vs computed in the table build (step0)
 OUT=gpurun_out/r02zf; mkdir -p $OUT
 python -m paper_2412_11614_b200.build > $OUT/build.log 2>&1
