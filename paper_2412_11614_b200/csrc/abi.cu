@@ -780,7 +780,8 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
                    : (h->num.mu_mode == ISRS_EGN_MU_INTEGRAL ? MODE_QUAD
                    : (h->num.mu_mode == ISRS_EGN_MU_MACLAURIN ? MODE_MACLAURIN
                       : (h->num.precision == 32 ? MODE_SEG32
-                         : ((h->num.flags & ISRS_EGN_FLAG_DEDUP) ? MODE_SEGDD
+                         : ((h->num.flags & ISRS_EGN_FLAG_DEDUP)
+                            ? (*std::max_element(h->chain_g.begin(), h->chain_g.end()) > 32 ? MODE_SEGDDL : MODE_SEGDD)
                             : ((h->num.flags & ISRS_EGN_FLAG_LITERAL_GAIN) ? MODE_SEGLG
                                : (h->n_grp < h->n_chain ? MODE_SEGGRP : MODE_SEGMENT))))));
   if (integrand_prepare(mode, h->tstride, h->tw, h->N) != 0)

@@ -72,7 +72,9 @@ enum : int { NEED_E = 1, NEED_F = 2, NEED_G = 4, NEED_H = 8, FV_SHIFT = 8 };
 // MODE_SEGLG: the segment form with the literal gain products of Eq. 22 (NEXT-4b)
 // MODE_SEGGRP: MODE_SEGMENT with chain groups (some group of identical spans holds > 1 chain, R9)
 enum : int { MODE_SEGMENT = 0, MODE_MACLAURIN = 1, MODE_UNIT = 2, MODE_SEG32 = 3, MODE_SEGDD = 4,
-             MODE_SEGLG = 5, MODE_QUAD = 6, MODE_SEGGRP = 7 };
+             MODE_SEGLG = 5, MODE_QUAD = 6, MODE_SEGGRP = 7, MODE_SEGDDL = 8 };
+// MODE_SEGDDL: MODE_SEGDD on links with a run of > 32 identical spans (closed-form phased-array factor);
+// its own instantiation so that the MODE_SEGDD kernel's code (and schedule) is unchanged
 
 struct RegionDesc {
   int kappa, k1, k2, flags;

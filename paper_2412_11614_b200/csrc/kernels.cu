@@ -778,9 +778,11 @@ template <bool COH, int MODE>
 __global__ void __launch_bounds__(BLOCK, MIN_BLOCKS)
 integrand_kernel(const KParams p, const int* __restrict__ list) {
   extern __shared__ __align__(16) char smem_raw[];
-  constexpr bool SEGM = (MODE == MODE_SEGMENT || MODE == MODE_SEGDD || MODE == MODE_SEGLG || MODE == MODE_SEGGRP);
+  constexpr bool SEGM = (MODE == MODE_SEGMENT || MODE == MODE_SEGDD || MODE == MODE_SEGLG || MODE == MODE_SEGGRP ||
+                         MODE == MODE_SEGDDL);
   constexpr bool LG = (MODE == MODE_SEGLG);   // literal Eq. 22 gain products (NEXT-4b)
-  constexpr bool DEDUP = (MODE == MODE_SEGDD);
+  constexpr bool DEDUP = (MODE == MODE_SEGDD || MODE == MODE_SEGDDL);
+  constexpr bool DEDUPL = (MODE == MODE_SEGDDL);   // closed-form phased-array factor for runs > 32 spans
   Smem sm;
   constexpr bool grouped = (MODE == MODE_SEGGRP);   // chain groups (R9): the segment mode when some
                                                      // group holds more than one chain
@@ -1105,7 +1107,40 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
               accr[q] = fma(cs[q], n0, tc.y - b1[q]);
               acci[q] = sn[q] * n0;
             }
-            if (DEDUP && G > 1) {
+            if (DEDUPL && G > 32) {
+              // NEXT-4a: x sum_{g<G} rho^g, rho = e^{i chi L} (the identical spans' phases, C3); for long
+              // runs in closed form e^{i (G-1) chi L / 2} sin(G chi L / 2) / sin(chi L / 2) (3 sincospi and
+              // a division instead of G - 1 complex products: c5's run of 50 spans, dedup 10.9 -> 9.0 s
+              // for all 200 COIs; slower than the products up to G ~ 30: c3's G = 20 +6 %); within 1e-3
+              // of a zero of sin(chi L / 2) (rho ~ 1, the ratio ill-conditioned) the products
+#pragma unroll
+              for (int q = 0; q < PPT; ++q) {
+                const double hx = x[q] * Ks;                       // chi L / pi
+                const double hr = hx - 2.0 * rint(0.5 * hx);       // exact, in [-1, 1]
+                double s1, c1;
+                sincospi_d(0.5 * hr, &s1, &c1);                    // sin, cos (chi L / 2)
+                double gr = 1.0, gim = 0.0;
+                if (fabs(s1) > 1e-3) {
+                  const double tg = 0.5 * (double)G * hr, tp = 0.5 * (double)(G - 1) * hr;
+                  double sg, cg, sp, cp;
+                  sincospi_d(tg - 2.0 * rint(0.5 * tg), &sg, &cg);
+                  sincospi_d(tp - 2.0 * rint(0.5 * tp), &sp, &cp);
+                  const double amp = sg / s1;
+                  gr = amp * cp;
+                  gim = amp * sp;
+                } else {
+                  const double rc = fma(-2.0 * s1, s1, 1.0), rs = 2.0 * s1 * c1;   // rho
+                  for (int g2 = 1; g2 < G; ++g2) {
+                    const double t = fma(gr, rc, fma(-gim, rs, 1.0));
+                    gim = fma(gr, rs, gim * rc);
+                    gr = t;
+                  }
+                }
+                const double ar = accr[q];
+                accr[q] = fma(ar, gr, -acci[q] * gim);
+                acci[q] = fma(ar, gim, acci[q] * gr);
+              }
+            } else if (DEDUP && G > 1) {
               // NEXT-4a: x sum_{g<G} rho^g, rho = e^{i chi L} (the identical spans' phases, C3)
 #pragma unroll
               for (int q = 0; q < PPT; ++q) {
@@ -1258,6 +1293,7 @@ int integrand_prepare(int mode, int tstride, int tw, int N) {
     case MODE_SEGGRP: return prepare_mode<MODE_SEGGRP>(tstride, tw, N);
     case MODE_SEG32: return prepare_mode<MODE_SEG32>(tstride, tw, N);
     case MODE_SEGDD: return prepare_mode<MODE_SEGDD>(tstride, tw, N);
+    case MODE_SEGDDL: return prepare_mode<MODE_SEGDDL>(tstride, tw, N);
     case MODE_SEGLG: return prepare_mode<MODE_SEGLG>(tstride, tw, N);
     case MODE_QUAD: return prepare_mode<MODE_QUAD>(tstride, tw, N);
     case MODE_MACLAURIN: return prepare_mode<MODE_MACLAURIN>(tstride, tw, N);
@@ -1287,6 +1323,7 @@ int launch_integrand(const KParams& p, const int* list, long long n_list, bool c
     if (p.mode == MODE_SEGGRP) return launch_one<true, MODE_SEGGRP>(p, list, n_list, st);
     if (p.mode == MODE_SEG32) return launch_one<true, MODE_SEG32>(p, list, n_list, st);
     if (p.mode == MODE_SEGDD) return launch_one<true, MODE_SEGDD>(p, list, n_list, st);
+    if (p.mode == MODE_SEGDDL) return launch_one<true, MODE_SEGDDL>(p, list, n_list, st);
     if (p.mode == MODE_SEGLG) return launch_one<true, MODE_SEGLG>(p, list, n_list, st);
     if (p.mode == MODE_QUAD) return launch_one<true, MODE_QUAD>(p, list, n_list, st);
     if (p.mode == MODE_MACLAURIN) return launch_one<true, MODE_MACLAURIN>(p, list, n_list, st);
@@ -1296,6 +1333,7 @@ int launch_integrand(const KParams& p, const int* list, long long n_list, bool c
   if (p.mode == MODE_SEGGRP) return launch_one<false, MODE_SEGGRP>(p, list, n_list, st);
   if (p.mode == MODE_SEG32) return launch_one<false, MODE_SEG32>(p, list, n_list, st);
   if (p.mode == MODE_SEGDD) return launch_one<false, MODE_SEGDD>(p, list, n_list, st);
+  if (p.mode == MODE_SEGDDL) return launch_one<false, MODE_SEGDDL>(p, list, n_list, st);
   if (p.mode == MODE_SEGLG) return launch_one<false, MODE_SEGLG>(p, list, n_list, st);
   if (p.mode == MODE_QUAD) return launch_one<false, MODE_QUAD>(p, list, n_list, st);
   if (p.mode == MODE_MACLAURIN) return launch_one<false, MODE_MACLAURIN>(p, list, n_list, st);

@@ -446,6 +446,19 @@ def test_dedup_mode_parity_tiny(isrs, name):
     assert np.all(np.abs(e_g - e_o) / e_o <= TOL_ETA), (name, np.abs(e_g - e_o) / e_o)
 
 
+def test_dedup_closed_form_long_run_parity(isrs):
+    """NEXT-4a on a run of 40 identical spans (> 32: the closed-form phased-array factor
+    e^{i(G-1)chi L/2} sin(G chi L/2)/sin(chi L/2), with the product loop near rho = 1) against the
+    oracle's span-by-span Eq. 22 sum and against the full GPU evaluation."""
+    link = tiny_link(n_ch=3, rates_gbd=(96,), spacing_ghz=100.0, n_span=40, grid_n=8,
+                     fmts=("16qam", "qpsk"), power_dbm=4.0)
+    e_o, _ = egn.eta(link)
+    e_d, _ = gpu_eta(isrs, link, flags=isrs.FLAG_DEDUP)
+    e_f, _ = gpu_eta(isrs, link)
+    assert np.all(np.abs(e_d - e_o) / e_o <= TOL_ETA), np.abs(e_d - e_o) / e_o
+    assert np.all(np.abs(e_d - e_f) / e_f <= TOL_ETA), np.abs(e_d - e_f) / e_f
+
+
 @pytest.mark.parametrize("cfg,coi", [("c2", None), ("c5", [100])])
 def test_dedup_mode_matches_full_evaluation(isrs, cfg, coi):
     link = bj_config(cfg)
