@@ -68,11 +68,17 @@ MUTANTS = {
     "cistab_cos_term": ("kernels.cu", "pc = fma(pc, r2, -4.934802200544679);",
                         "pc = fma(pc, r2, -4.934802200544679 * 0.999);",
                         "table sincospi: the r^2 coefficient of cos off by 0.1 %"),
+    # ---- NEXT-4a: the closed-form phased-array factor of long runs (MODE_SEGDDL)
+    "dedupl_phase_G": ("kernels.cu", "tp = 0.5 * (double)(G - 1) * hr;", "tp = 0.5 * (double)G * hr;",
+                       "dedup closed form: phase e^{i G chi L / 2} instead of e^{i (G-1) chi L / 2}"),
+    "dedupl_amp_cos": ("kernels.cu", "const double amp = sg / s1;", "const double amp = sg / c1;",
+                       "dedup closed form: sin(G chi L/2) / cos(chi L/2)"),
 }
 
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fvisibility=hidden", "-shared", "--expt-relaxed-constexpr"]
-TESTS = "tiny or edge or random_links or c1_full or streams or planned_work or chain_groups or (golden and c2_eta)"
+TESTS = ("tiny or edge or random_links or c1_full or streams or planned_work or chain_groups or (golden and c2_eta) "
+         "or dedup_closed_form")
 
 
 def _selected():
