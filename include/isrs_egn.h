@@ -26,6 +26,9 @@
  * on the caller's stream (cudaMallocAsync / cudaMemcpyAsync / cudaFreeAsync), after that stream has
  * been ordered behind the handle's previous call: no call synchronises the host or the device except
  * create (synchronous), destroy (synchronises the device) and the inspection calls that say so.
+ * An upload issued while that stream still has work in flight is staged in pinned host memory owned
+ * by the handle (a pageable source would hold the call until the stream reaches the copy), so such a
+ * call returns after the host planner's time; on an idle stream the source is pageable.
  * Errors: every call returns a status and isrs_egn_last_error() (thread-local) names the offending
  * field / index.  Validation, work-list limits, allocation and kernel attributes are checked before
  * the first kernel is enqueued, so on those errors no kernel runs and outputs are untouched (a work

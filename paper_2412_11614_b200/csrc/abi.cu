@@ -111,6 +111,57 @@ struct Arena {
   cudaStream_t st = nullptr;   // stream the allocation was made on (its free follows in that order)
 };
 
+// Pinned host staging for work-list uploads issued while the caller's stream is busy.  A pageable-
+// source cudaMemcpyAsync returns only once its data sits in the driver's staging buffer, and that
+// buffer stays occupied until the stream reaches the copy: the second upload behind a running kernel
+// blocked the host for the kernel's whole duration (tools/async_probe.py, profiles/r02zt_*).  From a
+// pinned source the copy is a plain stream-ordered DMA; the buffer is reused once the event recorded
+// behind its copy has completed, and buffers are only released by destroy (cudaFreeHost may
+// synchronise).  An idle stream takes the pageable path (no pinned allocation on the one-shot path).
+struct PinPool {
+  struct Buf {
+    char* p = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+    bool inflight = false;
+  };
+  std::vector<Buf> bufs;
+  bool busy() {   // some earlier upload from pinned memory has not completed yet
+    for (auto& b : bufs)
+      if (b.inflight) {
+        if (cudaEventQuery(b.ev) == cudaSuccess) b.inflight = false;
+        else { cudaGetLastError(); return true; }   // cudaErrorNotReady is not sticky; clear it
+      }
+    return false;
+  }
+  Buf* acquire(size_t bytes) {
+    for (auto& b : bufs) {
+      if (b.inflight && cudaEventQuery(b.ev) == cudaSuccess) b.inflight = false;
+      if (!b.inflight && b.cap >= bytes) return &b;
+    }
+    cudaGetLastError();
+    Buf b;
+    size_t cap = 1 << 16;
+    while (cap < bytes) cap <<= 1;
+    if (cudaHostAlloc((void**)&b.p, cap, cudaHostAllocDefault) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    if (cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFreeHost(b.p);
+      return nullptr;
+    }
+    b.cap = cap;
+    bufs.push_back(b);
+    return &bufs.back();
+  }
+  void release_all() {   // destroy only (the device is synchronised first)
+    for (auto& b : bufs) {
+      if (b.ev) cudaEventDestroy(b.ev);
+      if (b.p) cudaFreeHost(b.p);
+    }
+    bufs.clear();
+  }
+};
+
 class Packer {
   struct E {
     std::function<void(char*)> bind;
@@ -136,7 +187,9 @@ class Packer {
   // cudaMemcpyAsync returns once the data is staged, so the host vectors may die on return).  Only
   // when both succeed is the old arena freed (on `st`, which the caller has ordered after its last
   // use) and are the DevBufs rebound: on failure the handle keeps its previous, valid buffers.
-  cudaError_t commit(Arena* a, cudaStream_t st) {
+  // `pins` (the nli path): when `st` still has work in flight the upload is staged in pinned memory
+  // so that the call returns without waiting for that work.
+  cudaError_t commit(Arena* a, cudaStream_t st, PinPool* pins = nullptr) {
     size_t off = 0;
     for (auto& e : init_) { e.off = off; off += up(e.bytes); }
     const size_t init_bytes = off;
@@ -145,10 +198,25 @@ class Packer {
     cudaError_t ce = dev_alloc_on(&q, std::max<size_t>(off, 256), st);
     if (ce != cudaSuccess) return ce;
     if (init_bytes) {
-      std::vector<char> stage(init_bytes);
+      PinPool::Buf* pb = nullptr;
+      if (pins) {
+        bool stream_busy = pins->busy();
+        if (!stream_busy && cudaStreamQuery(st) != cudaSuccess) {
+          cudaGetLastError();
+          stream_busy = true;
+        }
+        if (stream_busy) pb = pins->acquire(init_bytes);   // NULL (no pinned memory): pageable path
+      }
+      std::vector<char> stage(pb ? 0 : init_bytes);
+      char* src = pb ? pb->p : stage.data();
       for (auto& e : init_)
-        if (e.bytes) std::memcpy(stage.data() + e.off, e.src, e.bytes);
-      ce = cudaMemcpyAsync(q, stage.data(), init_bytes, cudaMemcpyHostToDevice, st);
+        if (e.bytes) std::memcpy(src + e.off, e.src, e.bytes);
+      ce = cudaMemcpyAsync(q, src, init_bytes, cudaMemcpyHostToDevice, st);
+      if (ce == cudaSuccess && pb) {
+        ce = cudaEventRecord(pb->ev, st);
+        if (ce == cudaSuccess) pb->inflight = true;
+        else cudaStreamSynchronize(st);   // cannot track the copy: wait for it before the buffer is reused
+      }
       if (ce != cudaSuccess) {
         dev_free_on(q, st);
         return ce;
@@ -212,6 +280,7 @@ struct isrs_egn {
   DevBuf<int> d_sh_d, d_sh_c;
   DevBuf<double> d_partials, d_npts;
   Arena arena_create, arena_plan, arena_shard;
+  PinPool pins;   // pinned staging of work-list / shard-list uploads behind in-flight work
   cudaStream_t last_stream = nullptr;
   bool have_result = false;   // the partials hold the last call's values
   bool ordered = false;       // ev[3] marks the end of the handle's last direct call (on last_stream)
@@ -227,6 +296,7 @@ struct isrs_egn {
   ~isrs_egn() {   // isrs_egn_destroy synchronises the device first
     for (Arena* a : {&arena_plan, &arena_shard, &arena_create})
       if (a->base) cudaFreeAsync(a->base, 0);
+    pins.release_all();
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : evc)
@@ -803,7 +873,7 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
     pk.add(&list_d, wl.list_d); pk.add(&list_c, wl.list_c); pk.add(&fv, wl.fv);
     pk.reserve(&partials, wl.desc.size() * 6);
     pk.reserve(&npts, c.size());
-    ce = pk.commit(&h->arena_plan, st);      // on failure the handle keeps its previous work list
+    ce = pk.commit(&h->arena_plan, st, &h->pins);      // on failure the handle keeps its previous work list
     if (ce != cudaSuccess) return fail(ISRS_EGN_ENOMEM, std::string("work-list allocation failed: ") + cudaGetErrorString(ce));
     h->d_desc = desc; h->d_coi_off = coi_off; h->d_coi = coi_d; h->d_list_d = list_d;
     h->d_list_c = list_c; h->d_fv = fv; h->d_partials = partials; h->d_npts = npts;
@@ -832,7 +902,7 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
       DevBuf<int> sd, sc;
       pk.add(&sd, act_d);
       pk.add(&sc, act_c);
-      ce = pk.commit(&h->arena_shard, st);
+      ce = pk.commit(&h->arena_shard, st, &h->pins);
       if (ce != cudaSuccess) return fail(ISRS_EGN_ENOMEM, std::string("shard list allocation failed: ") + cudaGetErrorString(ce));
       h->d_sh_d = sd;
       h->d_sh_c = sc;
