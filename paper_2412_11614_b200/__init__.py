@@ -17,7 +17,7 @@ from ._abi import (FLAG_DEDUP, FLAG_LITERAL_GAIN, FLAG_MIRROR, FLAG_NO_CHAIN, FL
                    IsrsEgnError, ProblemArrays,  # noqa: F401
                    numerics)
 
-__all__ = ["Engine", "NliGraph", "eta_host", "plan_shards", "IsrsEgnError", "MU_SEGMENT", "MU_MACLAURIN", "MU_INTEGRAL", "FLAG_UNIT_LINK", "FLAG_NO_CHAIN", "FLAG_DEDUP", "FLAG_LITERAL_GAIN", "FLAG_MIRROR",
+__all__ = ["Engine", "Problem", "NliGraph", "eta_host", "plan_shards", "IsrsEgnError", "MU_SEGMENT", "MU_MACLAURIN", "MU_INTEGRAL", "FLAG_UNIT_LINK", "FLAG_NO_CHAIN", "FLAG_DEDUP", "FLAG_LITERAL_GAIN", "FLAG_MIRROR",
            "library_path"]
 
 
@@ -249,6 +249,74 @@ class NliGraph:
             self.close()
         except Exception:
             pass
+
+
+class Problem:
+    """A link description with the fields of `isrs_egn_problem` / `isrs_egn_numerics` (SI units, absolute
+    frequencies in integer Hz; include/isrs_egn.h).  Pure marshalling: values are passed through as given.
+
+        p = Problem.from_config("link.json")       # or a dict / a JSON string
+        with Engine(p) as e: eta = e.nli()
+
+    Config keys: the per-channel arrays f_center_hz, symbol_rate_hz, launch_power_w, excess_kurtosis
+    (optional psi), the per-span entries length_m, alpha_per_m, beta2_s2_per_m, beta3_s3_per_m,
+    gamma_per_w_m, cr_per_w_m_hz -- each a list of n_span values, or one number repeated for the
+    config's "n_span" identical spans -- and grid_n (optional delta_z_m, default 1000 m)."""
+
+    CHANNEL = ("f_center_hz", "symbol_rate_hz", "launch_power_w", "excess_kurtosis")
+    SPAN = ("length_m", "alpha_per_m", "beta2_s2_per_m", "beta3_s3_per_m", "gamma_per_w_m", "cr_per_w_m_hz")
+
+    def __init__(self, grid_n, delta_z_m=1000.0, psi=None, n_span=None, name="problem", **fields):
+        missing = [k for k in self.CHANNEL + self.SPAN if k not in fields]
+        unknown = [k for k in fields if k not in self.CHANNEL + self.SPAN]
+        if missing or unknown:
+            raise ValueError(f"Problem: missing {missing}, unknown {unknown}")
+        for k in self.CHANNEL:
+            setattr(self, k, np.ascontiguousarray(np.atleast_1d(np.asarray(fields[k], dtype=np.float64))))
+        n_ch = self.f_center_hz.size
+        if any(getattr(self, k).shape != (n_ch,) for k in self.CHANNEL):
+            raise ValueError("Problem: the per-channel arrays must all have n_ch entries")
+        self.psi = None if psi is None else np.ascontiguousarray(np.asarray(psi, dtype=np.float64))
+        if self.psi is not None and self.psi.shape != (n_ch,):
+            raise ValueError("Problem: psi must have n_ch entries")
+        sizes = {np.size(fields[k]) for k in self.SPAN if np.ndim(fields[k]) > 0}
+        if len(sizes) > 1 or (sizes and n_span is not None and sizes != {int(n_span)}):
+            raise ValueError("Problem: the per-span arrays must all have n_span entries")
+        ns = sizes.pop() if sizes else int(n_span if n_span is not None else 1)
+        for k in self.SPAN:
+            v = np.asarray(fields[k], dtype=np.float64)
+            setattr(self, k, np.ascontiguousarray(np.full(ns, float(v)) if v.ndim == 0 else v.reshape(ns)))
+        self.phi = self.excess_kurtosis          # the name Engine / ProblemArrays read
+        self.grid_n = int(grid_n)
+        self.delta_z_m = float(delta_z_m)
+        self.name = name
+
+    n_ch = property(lambda self: int(self.f_center_hz.size))
+    n_span = property(lambda self: int(self.length_m.size))
+
+    @classmethod
+    def from_config(cls, cfg):
+        """cfg: a dict, a JSON string, or the path of a JSON file."""
+        import json
+        import os
+        if isinstance(cfg, (str, bytes, os.PathLike)):
+            text = cfg.decode() if isinstance(cfg, bytes) else os.fspath(cfg)
+            if text.lstrip().startswith("{"):
+                cfg = json.loads(text)
+            else:
+                with open(text) as fh:
+                    cfg = json.load(fh)
+        if not isinstance(cfg, dict):
+            raise TypeError("Problem.from_config: a dict, a JSON string or a JSON file path")
+        return cls(**cfg)
+
+    def to_config(self):
+        """The dict `from_config` accepts (lists of Python floats: JSON-serialisable, exact round trip)."""
+        d = {k: getattr(self, k).tolist() for k in self.CHANNEL + self.SPAN}
+        if self.psi is not None:
+            d["psi"] = self.psi.tolist()
+        d.update(grid_n=self.grid_n, delta_z_m=self.delta_z_m, name=self.name)
+        return d
 
 
 def plan_shards(link, world, coi=None, grid_n=None, delta_z_m=None, f_samples=0):

@@ -136,3 +136,39 @@ def test_c_example_compiles_against_the_header_and_library(abi, tmp_path):
     libisrs_egn.so (it runs in tests/test_parity_gpu.py::test_c_example_matches_oracle)."""
     from _helpers import compile_c_example
     compile_c_example(str(tmp_path / "eta_c_abi"))
+
+
+def test_problem_from_config_marshals_the_same_struct(tmp_path):
+    """SURVEY 8(b) Python layer: Problem.from_config (dict / JSON string / JSON file, scalars repeated for
+    n_span identical spans) hands the C ABI exactly the arrays of the equivalent workloads Link, and the
+    host planner (no device) returns the same shard plan for both."""
+    import json
+
+    import paper_2412_11614_b200 as isrs
+    from paper_2412_11614_b200._abi import ProblemArrays
+    from workloads import tiny_link
+
+    link = tiny_link(n_ch=4, rates_gbd=(32, 64), guard_ghz=12.5, n_span=3, grid_n=8, fmts=("qpsk", "16qam"))
+    cfg = dict(f_center_hz=link.f_center_hz.tolist(), symbol_rate_hz=link.symbol_rate_hz.tolist(),
+               launch_power_w=link.launch_power_w.tolist(), excess_kurtosis=link.phi.tolist(),
+               psi=link.psi.tolist(), n_span=3, length_m=float(link.length_m[0]),
+               alpha_per_m=float(link.alpha_per_m[0]), beta2_s2_per_m=float(link.beta2_s2_per_m[0]),
+               beta3_s3_per_m=float(link.beta3_s3_per_m[0]), gamma_per_w_m=link.gamma_per_w_m.tolist(),
+               cr_per_w_m_hz=link.cr_per_w_m_hz.tolist(), grid_n=8, delta_z_m=link.delta_z_m)
+    path = tmp_path / "link.json"
+    path.write_text(json.dumps(cfg))
+    for src in (cfg, json.dumps(cfg), path, str(path)):
+        p = isrs.Problem.from_config(src)
+        a, b = ProblemArrays(p), ProblemArrays(link)
+        assert a.struct.n_ch == b.struct.n_ch == 4 and a.struct.n_span == b.struct.n_span == 3
+        for k in ProblemArrays.FIELDS:
+            assert np.array_equal(a._keep[k], b._keep[k]), k
+        assert isrs.Problem.from_config(json.dumps(p.to_config())).to_config() == p.to_config()
+    for x, y in zip(isrs.plan_shards(p, 2), isrs.plan_shards(link, 2)):
+        assert np.array_equal(x, y)
+    with pytest.raises(ValueError):
+        isrs.Problem.from_config({k: v for k, v in cfg.items() if k != "length_m"})
+    with pytest.raises(ValueError):
+        isrs.Problem.from_config(dict(cfg, alpha_db_km=0.2))
+    with pytest.raises(ValueError):
+        isrs.Problem.from_config(dict(cfg, length_m=[80e3, 80e3]))

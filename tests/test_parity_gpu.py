@@ -656,6 +656,24 @@ def test_coi_set_changes_return_before_the_gpu_finishes(isrs):
     assert t_issue < 0.15 * t_all, (t_issue, t_all)
 
 
+def test_problem_from_config_runs_the_same_eta(isrs):
+    """The binding's Problem.from_config (SURVEY 8(b) Python layer) drives the same hot path: eta is
+    bitwise the Link's, through a JSON round trip."""
+    import json
+    link = tiny_link(**TINY["mixed_rates_guard"])
+    ref, tref = gpu_eta(isrs, link)
+    p = isrs.Problem.from_config(json.dumps(dict(
+        f_center_hz=link.f_center_hz.tolist(), symbol_rate_hz=link.symbol_rate_hz.tolist(),
+        launch_power_w=link.launch_power_w.tolist(), excess_kurtosis=link.phi.tolist(), psi=link.psi.tolist(),
+        length_m=link.length_m.tolist(), alpha_per_m=link.alpha_per_m.tolist(),
+        beta2_s2_per_m=link.beta2_s2_per_m.tolist(), beta3_s3_per_m=link.beta3_s3_per_m.tolist(),
+        gamma_per_w_m=link.gamma_per_w_m.tolist(), cr_per_w_m_hz=link.cr_per_w_m_hz.tolist(),
+        grid_n=link.grid_n, delta_z_m=link.delta_z_m)))
+    eta, terms = gpu_eta(isrs, p)
+    assert np.array_equal(eta, ref) and np.array_equal(terms, tref)
+    assert np.array_equal(isrs.eta_host(p), ref)
+
+
 def test_planned_work_equals_the_kernels_count(isrs):
     """isrs_egn_work (host planner, no device) = isrs_egn_last_work (the kernels' own count)."""
     for link, coi in ((bj_config("c1"), None), (tiny_link(**TINY["touching_bands"]), [1, 2]),
