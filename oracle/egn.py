@@ -199,13 +199,21 @@ def island_contributions(c: Canon, k1: int, k2: int, isl: dict):
     return np.array([tD, tE, tF, tG, tH])
 
 
+def nli_class(kappa: int, k1: int, k2: int, k3: int) -> int:
+    """an island is SCI (0) when it involves the COI alone, XCI (1) when it involves ONE
+    interfering channel, MCI (2) when it involves two or three: the number of distinct channels of
+    (k1, k2, k3) other than the COI."""
+    return min(2, len({k1, k2, k3} - {kappa}))
+
+
 def eta(link, coi=None, mu_mode: str = "closed", return_regions: bool = False, f_samples: int = 0,
-        gain: str = "ideal"):
+        gain: str = "ideal", split: bool = False):
     """eta_kappa (1/W^2, Eq. 11 with P = P_kappa, reading C13) and the D/E/F/G/H breakdown.
 
     Brute force over every (kappa1, kappa2) pair and every grid point (Eq. 16 generalised to
     arbitrary channel plans: an island exists wherever f3 lands in a band).  f_samples > 0: the
     3-D form (NEXT-3), G_NLI averaged over f_samples midpoints of the COI band (coi_frequencies).
+    split=True also returns [n_coi, 3]: eta's SCI / XCI / MCI parts (nli_class), island by island.
     """
     c = canonicalize(link)
     n = c.f.size
@@ -213,8 +221,10 @@ def eta(link, coi=None, mu_mode: str = "closed", return_regions: bool = False, f
     etas = np.zeros(len(coi))
     terms = np.zeros((len(coi), 5))
     regions = {}
+    parts = np.zeros((len(coi), 3))
     for ci, kappa in enumerate(coi):
         acc = np.zeros(5)
+        cls = np.zeros(3)
         fs = coi_frequencies(c, kappa, f_samples)
         for f in fs:
             for k1 in range(n):
@@ -227,13 +237,18 @@ def eta(link, coi=None, mu_mode: str = "closed", return_regions: bool = False, f
                     if return_regions:
                         regions[(kappa, k1, k2) if f_samples <= 0 else (kappa, float(f), k1, k2)] = isls
                     for isl in isls:
-                        acc = acc + island_contributions(c, k1, k2, isl)
+                        contrib = island_contributions(c, k1, k2, isl)
+                        acc = acc + contrib
+                        cls[nli_class(kappa, k1, k2, isl["k3"])] += contrib.sum()
         # P_NLI = R G_NLI(f_kappa) (C1) or sum_m G_NLI(f_m) R / n (3-D); Eq. 11
         scale = c.R[kappa] / c.P[kappa] ** 3 / len(fs)
         terms[ci] = acc * scale
         etas[ci] = acc.sum() * scale
+        parts[ci] = cls * scale
     if return_regions:
         return etas, terms, regions
+    if split:
+        return etas, terms, parts
     return etas, terms
 
 
@@ -307,6 +322,6 @@ def unit_link_eta(phi, psi):
 
 
 __all__ = ["Canon", "canonicalize", "grid", "region_points", "island_gates", "region_islands",
-           "island_contributions", "eta", "region_partials", "eta_db", "unit_link_eta",
+           "island_contributions", "nli_class", "eta", "region_partials", "eta_db", "unit_link_eta",
            "unit_link_eta_3d", "coi_frequencies",
            "has_support_bound", "math"]

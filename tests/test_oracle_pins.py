@@ -539,3 +539,39 @@ def test_support_bound_filter_drops_only_empty_regions(name, monkeypatch):
                 _, _, f3 = egn.region_points(c, k, a, b)
                 has = any(np.any((f3 >= c.lo[i]) & (f3 <= c.hi[i])) for i in range(link.n_ch))
                 assert has == ((k, a, b) in kept), (name, k, a, b, has)
+
+
+# ---------------------------------------------------------------- SCI / XCI / MCI split
+
+def test_P17_sci_xci_mci_split():
+    """SCI = the COI alone, XCI = one interfering channel, MCI = two or three.  Pins: the three
+    parts sum to eta; a single channel has only SCI; two channels have no MCI (only one interferer
+    exists) but do have XCI; with C_r = 0 the SCI of the middle channel of a symmetric 3-channel link
+    (same band centre f_c, no ISRS coupling to the neighbours) IS the eta of that channel alone --
+    although at 96 GBd on 100 GHz its (kappa, kappa) region also holds kappa3 = kappa +- 1 islands,
+    which are XCI; and the split of Eq. 16's island set for M = 1, kappa = 0 counted by hand."""
+    kw = dict(rates_gbd=(96,), spacing_ghz=100.0, n_span=2, grid_n=8, fmts=("16qam",))
+    l3 = tiny_link(n_ch=3, **kw)
+    e, t, s = egn.eta(l3, split=True)
+    assert np.allclose(s.sum(axis=1), e, rtol=1e-13, atol=0)
+    assert np.all(s > 0)
+    e1, _, s1 = egn.eta(tiny_link(n_ch=1, **kw), split=True)
+    assert s1[0, 1] == 0.0 and s1[0, 2] == 0.0 and s1[0, 0] == e1[0]
+    e2, _, s2 = egn.eta(tiny_link(n_ch=2, **kw), split=True)
+    assert np.all(s2[:, 2] == 0.0) and np.all(s2[:, 1] > 0)
+    # C_r = 0: SCI of the middle channel = eta of that channel alone (same f_c)
+    l3n = l3.with_(cr_per_w_m_hz=np.zeros(2))
+    mid = l3n.with_(f_center_hz=l3n.f_center_hz[1:2], symbol_rate_hz=l3n.symbol_rate_hz[1:2],
+                    launch_power_w=l3n.launch_power_w[1:2], phi=l3n.phi[1:2], psi=l3n.psi[1:2])
+    _, _, s3 = egn.eta(l3n, coi=[1], split=True)
+    e_mid, _ = egn.eta(mid)
+    assert abs(s3[0, 0] - e_mid[0]) <= 1e-13 * e_mid[0]
+    isl = egn.island_set_generalised(l3n, 1)                   # the (1, 1) region holds three islands
+    assert sorted(k3 for k1, k2, k3 in isl if k1 == k2 == 1) == [0, 1, 2]
+    # Eq. 16 with M = 1, kappa = 0 (channels -1, 0, 1), by hand: of its 19 islands (k1, k2, k3 = k1+k2+l)
+    # 1 is SCI (0,0,0); XCI are the islands over {0, j} with j = +-1 present: (0,0,j), (0,j,0), (j,0,0),
+    # (0,j,j), (j,0,j), (j,j,0)*, (j,j,j) -- (j,j,0) needs l = -2j, not in {-1,0,1} -- so 6 per j = 12
+    cnt = [0, 0, 0]
+    for k1, k2, ll in egn.island_set_eq16(1, 0):
+        cnt[egn.nli_class(0, k1, k2, k1 + k2 - 0 + ll)] += 1
+    assert cnt == [1, 12, 6]
