@@ -110,12 +110,22 @@ enum { ISRS_EGN_FLAG_UNIT_LINK = 1u, /* test hook: Y := 1 (oracle pin P6)       
                                         (mean loss restored, SRS tilt persists) instead of reading C3's
                                         ideal per-frequency equalisation (products = 1); fp64 segment
                                         mode only */
-       ISRS_EGN_FLAG_MIRROR = 16u    /* f1 <-> f2 symmetry (Eqs. 5, 8, 22 and the gates are symmetric in
+       ISRS_EGN_FLAG_MIRROR = 16u,   /* f1 <-> f2 symmetry (Eqs. 5, 8, 22 and the gates are symmetric in
                                         f1, f2; pin P2): region (kappa, k1, k2), k1 < k2, is evaluated once
                                         and also yields (kappa, k2, k1) with E and F exchanged -- about half
                                         the point-spans evaluated, the same eta.  Like DEDUP its rate is
                                         reported separately (logical point-spans), never as the headline.
-                                        Not with isrs_egn_nli_shard (EUNSUPPORTED). */ };
+                                        Not with isrs_egn_nli_shard (EUNSUPPORTED). */
+       ISRS_EGN_FLAG_SPLIT = 32u     /* SCI / XCI / MCI parts of eta (interference from the COI alone,
+                                        from one interfering channel, from two or three), returned by
+                                        isrs_egn_nli_split.  An island (k1, k2, k3) belongs to the class given
+                                        by the number of distinct channels among k1, k2, k3 other than the COI;
+                                        a region whose islands fall into two classes is evaluated as two work-list
+                                        entries, each over the lattice lines of one class (same points, same
+                                        eta up to summation order).  fp64 segment mode only, not with DEDUP,
+                                        LITERAL_GAIN, MIRROR, UNIT_LINK or shards (EUNSUPPORTED);
+                                        isrs_egn_region_partials then sums a region's two entries, and a point on
+                                        an edge shared by bands of both classes is counted in both entries. */ };
 
 typedef struct {
   int32_t grid_n;      /* N: N x N bin-centre grid per (kappa1, kappa2) region; even, >= 2 (C6) */
@@ -142,6 +152,12 @@ ISRS_EGN_API int isrs_egn_create(const isrs_egn_problem *p, const isrs_egn_numer
  * bitwise-identical results across calls. */
 ISRS_EGN_API int isrs_egn_nli(isrs_egn_t *h, int32_t n_coi, const int32_t *coi, double *eta_dev,
                  double *terms_dev, void *cuda_stream);
+
+/* isrs_egn_nli plus the SCI / XCI / MCI parts of eta (the handle must have been created with
+ * ISRS_EGN_FLAG_SPLIT, else EINVAL): split_dev DEVICE [n_coi * 3], row-major {SCI, XCI, MCI} in 1/W^2,
+ * eta = SCI + XCI + MCI up to rounding.  Same asynchrony and determinism as isrs_egn_nli. */
+ISRS_EGN_API int isrs_egn_nli_split(isrs_egn_t *h, int32_t n_coi, const int32_t *coi, double *eta_dev,
+                 double *terms_dev, double *split_dev, void *cuda_stream);
 
 /* ---- Multi-GPU: one process and one handle per GPU.  The canonical region list of
  * the COI set (COI, f sample, k1, k2 order) is split into `world` contiguous shards of near-equal cost

@@ -13,11 +13,11 @@ import ctypes
 import numpy as np
 
 from . import _abi
-from ._abi import (FLAG_DEDUP, FLAG_LITERAL_GAIN, FLAG_MIRROR, FLAG_NO_CHAIN, FLAG_UNIT_LINK, MU_INTEGRAL, MU_MACLAURIN, MU_SEGMENT,
+from ._abi import (FLAG_DEDUP, FLAG_LITERAL_GAIN, FLAG_MIRROR, FLAG_NO_CHAIN, FLAG_SPLIT, FLAG_UNIT_LINK, MU_INTEGRAL, MU_MACLAURIN, MU_SEGMENT,
                    IsrsEgnError, ProblemArrays,  # noqa: F401
                    numerics)
 
-__all__ = ["Engine", "Problem", "NliGraph", "eta_host", "plan_shards", "IsrsEgnError", "MU_SEGMENT", "MU_MACLAURIN", "MU_INTEGRAL", "FLAG_UNIT_LINK", "FLAG_NO_CHAIN", "FLAG_DEDUP", "FLAG_LITERAL_GAIN", "FLAG_MIRROR",
+__all__ = ["Engine", "Problem", "NliGraph", "eta_host", "plan_shards", "IsrsEgnError", "MU_SEGMENT", "MU_MACLAURIN", "MU_INTEGRAL", "FLAG_UNIT_LINK", "FLAG_NO_CHAIN", "FLAG_DEDUP", "FLAG_LITERAL_GAIN", "FLAG_MIRROR", "FLAG_SPLIT",
            "library_path"]
 
 
@@ -71,6 +71,22 @@ class Engine:
         st = stream if stream is not None else torch.cuda.current_stream(dev)
         self.nli_into(eta.data_ptr(), tt.data_ptr() if terms else 0, coi, st.cuda_stream)
         return (eta, tt) if terms else eta
+
+    def nli_split(self, coi=None, terms=False, stream=None):
+        """isrs_egn_nli_split (an Engine created with flags=FLAG_SPLIT): eta [n_coi], its SCI / XCI / MCI
+        parts [n_coi, 3] and, with terms=True, the D..H breakdown [n_coi, 5]."""
+        import torch
+        n, cp = self._coi(coi)
+        dev = torch.device("cuda", self.device)
+        eta = torch.empty(n, dtype=torch.float64, device=dev)
+        parts = torch.empty((n, 3), dtype=torch.float64, device=dev)
+        tt = torch.empty((n, 5), dtype=torch.float64, device=dev) if terms else None
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        _abi.check(_abi.get().isrs_egn_nli_split(self._h, n, cp, ctypes.c_void_p(eta.data_ptr()),
+                                               ctypes.c_void_p(tt.data_ptr() if terms else None),
+                                               ctypes.c_void_p(parts.data_ptr()),
+                                               ctypes.c_void_p(st.cuda_stream or None)))
+        return (eta, parts, tt) if terms else (eta, parts)
 
     def region_partials(self, regions):
         """[(kappa, k1, k2), ...] -> array [n, 6]: D_w, E_w, F_w, G_w, H_w, n_points (last call)."""

@@ -19,8 +19,9 @@ FLAG_NO_CHAIN = 2
 FLAG_DEDUP = 4
 FLAG_LITERAL_GAIN = 8
 FLAG_MIRROR = 16
+FLAG_SPLIT = 32
 
-EXPORTED = ("isrs_egn_create", "isrs_egn_nli", "isrs_egn_region_partials", "isrs_egn_work", "isrs_egn_last_work",
+EXPORTED = ("isrs_egn_create", "isrs_egn_nli", "isrs_egn_nli_split", "isrs_egn_region_partials", "isrs_egn_work", "isrs_egn_last_work",
             "isrs_egn_eta_host", "isrs_egn_last_kernel_ms", "isrs_egn_last_launch_count",
             "isrs_egn_span_chains", "isrs_egn_chain_groups", "isrs_egn_profile_tables", "isrs_egn_nli_shard", "isrs_egn_combine", "isrs_egn_plan_shards",
             "isrs_egn_destroy",
@@ -62,6 +63,9 @@ def _load():
     lib.isrs_egn_nli.argtypes = [ctypes.c_void_p, ctypes.c_int32, _ip, ctypes.c_void_p,
                                  ctypes.c_void_p, ctypes.c_void_p]
     lib.isrs_egn_nli.restype = ctypes.c_int
+    lib.isrs_egn_nli_split.argtypes = [ctypes.c_void_p, ctypes.c_int32, _ip, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    lib.isrs_egn_nli_split.restype = ctypes.c_int
     lib.isrs_egn_region_partials.argtypes = [ctypes.c_void_p, ctypes.c_int32, _ip, _ip, _ip, _dp]
     lib.isrs_egn_region_partials.restype = ctypes.c_int
     lib.isrs_egn_chain_groups.argtypes = [ctypes.c_void_p, _ip, _ip]

@@ -328,6 +328,10 @@ static int validate(const isrs_egn_problem* p, const isrs_egn_numerics* n) {
   if ((n->flags & ISRS_EGN_FLAG_LITERAL_GAIN) &&
       (n->mu_mode != ISRS_EGN_MU_SEGMENT || n->precision == 32 || (n->flags & ISRS_EGN_FLAG_DEDUP)))
     return fail(ISRS_EGN_EUNSUPPORTED, "LITERAL_GAIN is an fp64 segment-mode variant (no DEDUP)");
+  if ((n->flags & ISRS_EGN_FLAG_SPLIT) &&
+      (n->mu_mode != ISRS_EGN_MU_SEGMENT || n->precision == 32 ||
+       (n->flags & (ISRS_EGN_FLAG_DEDUP | ISRS_EGN_FLAG_LITERAL_GAIN | ISRS_EGN_FLAG_MIRROR | ISRS_EGN_FLAG_UNIT_LINK))))
+    return fail(ISRS_EGN_EUNSUPPORTED, "SPLIT is an fp64 segment-mode option (no DEDUP, LITERAL_GAIN, MIRROR, UNIT_LINK)");
   if (n->f_samples < 0 || n->f_samples > 4096) return fail(ISRS_EGN_EINVAL, "f_samples must be in [0, 4096]");
   if (n->mu_mode != ISRS_EGN_MU_SEGMENT && n->mu_mode != ISRS_EGN_MU_MACLAURIN &&
       n->mu_mode != ISRS_EGN_MU_INTEGRAL)
@@ -670,7 +674,8 @@ static long long ceil_div(long long x, long long y) { return -floor_div(-x, y); 
 // lattice_cum(j1) - lattice_cum(j0 - 1).  All frequencies are multiples of 1/4 Hz (integer-Hz inputs,
 // f_c the midpoint of half-integer edges), so the interval ends are computed in exact integers.
 // O(bands x (1 or N)) per region instead of a walk over every point.
-static long long region_points(const isrs_egn* h, double f, int k1, int k2) {
+// `filter` (ISRS_EGN_FLAG_SPLIT): 0 every band, K3_IN only the bands kappa, k1, k2, K3_OUT only the others.
+static long long region_points(const isrs_egn* h, double f, int k1, int k2, int kappa = -1, int filter = 0) {
   const int N = h->N, nc = h->n_ch;
   const long long r1 = h->rate[k1], r2 = h->rate[k2];
   long long x = r1, y = r2;
@@ -686,6 +691,10 @@ static long long region_points(const isrs_egn* h, double f, int k1, int k2) {
   long long cnt = 0, cur0 = 0, cur1 = -2;     // current merged interval [cur0, cur1]
   for (int c = (int)(std::lower_bound(h->hi.begin(), h->hi.end(), C) - h->hi.begin());
        c < nc && h->lo[c] <= f3max; ++c) {
+    if (filter) {
+      const bool in = (c == kappa || c == k1 || c == k2);
+      if ((filter == K3_IN) != in) continue;
+    }
     const long long j0 = std::max(0LL, ceil_div(q4(h->lo[c]) - C4, g4));
     const long long j1 = std::min(J - 1, floor_div(q4(h->hi[c]) - C4, g4));
     if (j0 > j1) continue;
@@ -715,6 +724,7 @@ static void build_worklist(const isrs_egn* h, const std::vector<int>& coi, WorkL
   cost.clear();
   const int nc = h->n_ch;
   const bool mirror = (h->num.flags & ISRS_EGN_FLAG_MIRROR) != 0;
+  const bool split = (h->num.flags & ISRS_EGN_FLAG_SPLIT) != 0;
   std::vector<int> idmap;
   const int fs = h->num.f_samples, nfs = std::max(1, fs);
   for (int kappa : coi) {
@@ -739,6 +749,25 @@ static void build_worklist(const isrs_egn* h, const std::vector<int>& coi, WorkL
         if (h->phi[k2] != 0.0 && overlaps(k2)) flags |= NEED_F;
         if (h->phi[k1] != 0.0 && k1 == k2) flags |= NEED_G;
         if (h->psi[k1] != 0.0 && k1 == k2 && overlaps(k1)) flags |= NEED_H;
+        if (split && (k1 == kappa || k2 == kappa || k1 == k2)) {
+          // SCI / XCI / MCI: at most one interfering channel among (k1, k2), so the class of an
+          // island depends on whether k3 is one of {kappa, k1, k2}: one entry per class, each over its
+          // own lattice lines (E, F, H tie k3 to k1 / k2, so they live in the K3_IN entry; G follows D)
+          const long long pin = region_points(h, f, k1, k2, kappa, K3_IN);
+          const long long pout = region_points(h, f, k1, k2, kappa, K3_OUT);
+          if (pin > 0 || pout == 0) {
+            (flags ? w->list_c : w->list_d).push_back((int)w->desc.size());
+            w->desc.push_back(RegionDesc{kappa, k1, k2, flags | K3_IN | (fvi << FV_SHIFT)});
+            cost.push_back(pin);
+          }
+          if (pout > 0) {
+            const int fo = flags & NEED_G;
+            (fo ? w->list_c : w->list_d).push_back((int)w->desc.size());
+            w->desc.push_back(RegionDesc{kappa, k1, k2, fo | K3_OUT | (fvi << FV_SHIFT)});
+            cost.push_back(pout);
+          }
+          continue;
+        }
         const int id = (int)w->desc.size();
         w->desc.push_back(RegionDesc{kappa, k1, k2, flags | (fvi << FV_SHIFT)});
         cost.push_back(region_points(h, f, k1, k2));
@@ -813,7 +842,7 @@ static void shard_range(const WorkList& w, int rank, int world, long long* lo, l
 // While `st` is being captured into a CUDA graph the call only enqueues kernels (no allocation: the
 // work list must exist already, no timing or ordering events; fork / join use capture-only events).
 static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, double* eta_dev,
-                   double* terms_dev, double* part_out, cudaStream_t st) {
+                   double* terms_dev, double* part_out, cudaStream_t st, double* split_dev = nullptr) {
   DeviceGuard dg(h->device);
   if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
   cudaError_t ce = cudaGetLastError();
@@ -829,7 +858,8 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
                                  "on a non-capturing stream first, so that nothing is allocated inside the capture");
   if (rebuild) {
     // region ids are int32 and the f-sample index lives in 23 flag bits
-    const double nreg_max = (double)c.size() * std::max(1, h->num.f_samples) * h->n_ch * h->n_ch;
+    // (FLAG_SPLIT lists the < 3 n_ch regions with at most one interfering channel twice)
+    const double nreg_max = (double)c.size() * std::max(1, h->num.f_samples) * h->n_ch * ((double)h->n_ch + 3);
     if (nreg_max > 2147483647.0 || (double)c.size() * std::max(1, h->num.f_samples) >= 8388608.0)
       return fail(ISRS_EGN_ERANGE, "n_coi x f_samples x n_ch^2 regions exceed the 2^31 work-list limit");
   }
@@ -853,7 +883,9 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
                          : ((h->num.flags & ISRS_EGN_FLAG_DEDUP)
                             ? (*std::max_element(h->chain_g.begin(), h->chain_g.end()) > 32 ? MODE_SEGDDL : MODE_SEGDD)
                             : ((h->num.flags & ISRS_EGN_FLAG_LITERAL_GAIN) ? MODE_SEGLG
-                               : (h->n_grp < h->n_chain ? MODE_SEGGRP : MODE_SEGMENT))))));
+                               : ((h->num.flags & ISRS_EGN_FLAG_SPLIT)
+                                  ? (h->n_grp < h->n_chain ? MODE_SEGGRPSPL : MODE_SEGSPL)
+                                  : (h->n_grp < h->n_chain ? MODE_SEGGRP : MODE_SEGMENT)))))));
   if (integrand_prepare(mode, h->tstride, h->tw, h->N) != 0)
     return cuda_fail(cudaGetLastError(), "integrand kernel attributes");
   // calls on one handle share its partials (and a rebuild frees the previous work list): a call on
@@ -974,6 +1006,10 @@ static int run_nli(isrs_egn* h, const std::vector<int>& c, int rank, int world, 
              part_out};
   if (launch_reduce(rp, st) != 0) return cuda_fail(cudaGetLastError(), "reduce launch");
   launches += 1;
+  if (split_dev) {   // SCI / XCI / MCI parts from the same partials (ISRS_EGN_FLAG_SPLIT work list)
+    if (launch_reduce_split(rp, split_dev, st) != 0) return cuda_fail(cudaGetLastError(), "split reduce launch");
+    launches += 1;
+  }
   if (capturing) return ISRS_EGN_OK;     // the handle's timing / ordering state describes direct calls
   cudaEventRecord(h->ev[3], st);
   h->ordered = true;
@@ -1013,6 +1049,19 @@ extern "C" int isrs_egn_nli(isrs_egn_t* h, int32_t n_coi, const int32_t* coi, do
   return run_nli(h, c, 0, 1, eta_dev, terms_dev, nullptr, (cudaStream_t)cuda_stream);
 }
 
+extern "C" int isrs_egn_nli_split(isrs_egn_t* h, int32_t n_coi, const int32_t* coi, double* eta_dev,
+                                  double* terms_dev, double* split_dev, void* cuda_stream) {
+  if (!h) return fail(ISRS_EGN_EINVAL, "handle is NULL");
+  if (!eta_dev || !split_dev) return fail(ISRS_EGN_EINVAL, "eta_dev / split_dev is NULL");
+  if (!(h->num.flags & ISRS_EGN_FLAG_SPLIT))
+    return fail(ISRS_EGN_EINVAL, "isrs_egn_nli_split needs a handle created with ISRS_EGN_FLAG_SPLIT");
+  NvtxRange nv("isrs_egn_nli_split");
+  std::vector<int> c;
+  int rc = coi_list(h, n_coi, coi, &c);
+  if (rc) return rc;
+  return run_nli(h, c, 0, 1, eta_dev, terms_dev, nullptr, (cudaStream_t)cuda_stream, split_dev);
+}
+
 extern "C" int isrs_egn_nli_shard(isrs_egn_t* h, int32_t n_coi, const int32_t* coi, int32_t rank,
                                   int32_t world, double* coi_sums_dev, void* cuda_stream) {
   if (!h) return fail(ISRS_EGN_EINVAL, "handle is NULL");
@@ -1021,6 +1070,8 @@ extern "C" int isrs_egn_nli_shard(isrs_egn_t* h, int32_t n_coi, const int32_t* c
   if (world < 1 || rank < 0 || rank >= world) return fail(ISRS_EGN_EINVAL, "rank/world out of range");
   if (h->num.flags & ISRS_EGN_FLAG_MIRROR)
     return fail(ISRS_EGN_EUNSUPPORTED, "FLAG_MIRROR writes partner regions across the region list: no shards");
+  if (h->num.flags & ISRS_EGN_FLAG_SPLIT)
+    return fail(ISRS_EGN_EUNSUPPORTED, "FLAG_SPLIT: the SCI / XCI / MCI parts are not sharded");
   std::vector<int> c;
   int rc = coi_list(h, n_coi, coi, &c);
   if (rc) return rc;
@@ -1089,11 +1140,15 @@ extern "C" int isrs_egn_region_partials(isrs_egn_t* h, int32_t n, const int32_t*
     auto itc = std::find(w.coi.begin(), w.coi.end(), kappa[q]);
     if (itc == w.coi.end()) continue;
     const size_t ci = itc - w.coi.begin();
+    bool found = false;
     for (long long r = w.coi_off[ci]; r < w.coi_off[ci + 1]; ++r) {
       if (w.desc[r].k1 == k1[q] && w.desc[r].k2 == k2[q]) {
-        ce = cudaMemcpy(o, h->d_partials.p + r * 6, 6 * sizeof(double), cudaMemcpyDeviceToHost);
+        double v[6];
+        ce = cudaMemcpy(v, h->d_partials.p + r * 6, 6 * sizeof(double), cudaMemcpyDeviceToHost);
         if (ce != cudaSuccess) return cuda_fail(ce, "partials copy");
-        break;
+        for (int k = 0; k < 6; ++k) o[k] = found ? o[k] + v[k] : v[k];
+        found = true;
+        if (!(h->num.flags & ISRS_EGN_FLAG_SPLIT)) break;   // SPLIT: a region may have two entries
       }
     }
   }

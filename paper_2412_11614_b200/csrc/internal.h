@@ -65,6 +65,10 @@ static_assert(BLOCK % 32 == 0 && (BLOCK & (BLOCK - 1)) == 0 && BLOCK <= 1024,
 // hold the index of the region's NLI frequency f in KParams::fv (COI centre, or one of the
 // f samples of the 3-D form)
 enum : int { NEED_E = 1, NEED_F = 2, NEED_G = 4, NEED_H = 8, FV_SHIFT = 8 };
+// ISRS_EGN_FLAG_SPLIT (SCI / XCI / MCI parts of eta): a region (kappa, k1, k2) whose islands can
+// fall into two classes is listed twice, once restricted to the lattice lines whose k3 is one of
+// {kappa, k1, k2} (K3_IN) and once to the others (K3_OUT); MODE_SEGSPL / MODE_SEGGRPSPL apply the filter
+enum : int { K3_IN = 16, K3_OUT = 32 };
 
 // MODE_SEG32: row a8, the mixed fp32 variant of the segment form (fp32 recurrence, mu, phase
 // factor; fp64 chi h and its exact reduction, the phase advance and every accumulation)
@@ -72,7 +76,11 @@ enum : int { NEED_E = 1, NEED_F = 2, NEED_G = 4, NEED_H = 8, FV_SHIFT = 8 };
 // MODE_SEGLG: the segment form with the literal gain products of Eq. 22 (NEXT-4b)
 // MODE_SEGGRP: MODE_SEGMENT with chain groups (some group of identical spans holds > 1 chain, R9)
 enum : int { MODE_SEGMENT = 0, MODE_MACLAURIN = 1, MODE_UNIT = 2, MODE_SEG32 = 3, MODE_SEGDD = 4,
-             MODE_SEGLG = 5, MODE_QUAD = 6, MODE_SEGGRP = 7, MODE_SEGDDL = 8 };
+             MODE_SEGLG = 5, MODE_QUAD = 6, MODE_SEGGRP = 7, MODE_SEGDDL = 8, MODE_SEGSPL = 9,
+             MODE_SEGGRPSPL = 10 };
+// MODE_SEGSPL / MODE_SEGGRPSPL: MODE_SEGMENT / MODE_SEGGRP with the k3 line filter of the SCI / XCI / MCI
+// split; their own instantiations so that the headline kernels' code (and schedule) is unchanged
+constexpr bool mode_grouped(int mode) { return mode == MODE_SEGGRP || mode == MODE_SEGGRPSPL; }
 // MODE_SEGDDL: MODE_SEGDD on links with a run of > 32 identical spans (closed-form phased-array factor);
 // its own instantiation so that the MODE_SEGDD kernel's code (and schedule) is unchanged
 
@@ -202,6 +210,7 @@ int integrand_prepare(int mode, int tstride, int tw, int N);
 int launch_integrand(const KParams& p, const int* list, long long n_list, bool coherent,
                      void* stream, int* n_launches);
 int launch_reduce(const RParams& p, void* stream);
+int launch_reduce_split(const RParams& p, double* split_out, void* stream);
 int launch_combine(const CParams& p, void* stream);
 
 }  // namespace isrs

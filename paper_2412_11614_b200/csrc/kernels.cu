@@ -248,8 +248,11 @@ __device__ inline int line_of(const int* sl_start, int hi, int p, int lo = 0) {
 
 // f3-gate of one lattice line (reading C10): every band [lo, hi] containing f3 contributes
 // t = 1 strictly inside, 1/2 on an edge (touching bands split 1/2 / 1/2).
-__device__ inline void line_gate(const KParams& p, double f3, int k1, int k2, double* wD, double* wE,
-                                 double* wF) {
+// SPLIT (MODE_SEGSPL / MODE_SEGGRPSPL): only the bands c of the region entry's class count -- K3_IN:
+// c one of {kappa, k1, k2}, K3_OUT: the others (the SCI / XCI / MCI split).
+template <bool SPLIT>
+__device__ inline void line_gate(const KParams& p, double f3, int kappa, int k1, int k2, int flags, double* wD,
+                                 double* wE, double* wF) {
   double d = 0.0, e = 0.0, ff = 0.0;
   int lo = 0, hi = p.n_ch - 1;       // largest i with lo[i] <= f3
   if (f3 >= __ldg(p.lo)) {
@@ -260,6 +263,10 @@ __device__ inline void line_gate(const KParams& p, double f3, int k1, int k2, do
     for (int c = lo; c >= lo - 1 && c >= 0; --c) {
       const double l = __ldg(p.lo + c), h = __ldg(p.hi + c);
       if (f3 >= l && f3 <= h) {
+        if (SPLIT) {
+          const bool in = (c == kappa || c == k1 || c == k2);
+          if (((flags & K3_IN) && !in) || ((flags & K3_OUT) && in)) continue;
+        }
         const double t = (f3 > l && f3 < h) ? 1.0 : 0.5;
         d += t * __ldg(p.G + c);
         if (c == k1) e += t;
@@ -356,8 +363,10 @@ __device__ inline long long gcd_ll(long long a, long long b) {
 // C10 gate weights (line_gate) are per line; supported lines are compacted in order into sm.sl_*
 // with their slot offsets (each line padded to whole PPT-groups).  Returns (lines, slots, points).
 // All threads must call (block scan).
+template <bool SPLIT>
 __device__ __forceinline__ int4 scan_lines(const KParams& p, const Smem& sm, int seg0, int nl, int N, int a,
-                                           int b, int inv_a, int k1, int k2, double C, double g) {
+                                           int b, int inv_a, int kappa, int k1, int k2, int flags, double C,
+                                           double g) {
   const int tid = threadIdx.x;
   // ---- line scan: each thread owns LPT consecutive lines (order-preserving compaction)
   int cnt[LPT], first[LPT];
@@ -383,7 +392,7 @@ __device__ __forceinline__ int4 scan_lines(const KParams& p, const Smem& sm, int
       const int n = (fm <= upb) ? (upb - fm) / b + 1 : 0;
       if (n > 0) {
         const double f3 = __dadd_rn(C, g * (double)j);
-        line_gate(p, f3, k1, k2, &lwD[q], &lwE[q], &lwF[q]);
+        line_gate<SPLIT>(p, f3, kappa, k1, k2, flags, &lwD[q], &lwE[q], &lwF[q]);
         if (lwD[q] > 0.0) {
           cnt[q] = n;
           first[q] = fm;
@@ -779,12 +788,13 @@ __global__ void __launch_bounds__(BLOCK, MIN_BLOCKS)
 integrand_kernel(const KParams p, const int* __restrict__ list) {
   extern __shared__ __align__(16) char smem_raw[];
   constexpr bool SEGM = (MODE == MODE_SEGMENT || MODE == MODE_SEGDD || MODE == MODE_SEGLG || MODE == MODE_SEGGRP ||
-                         MODE == MODE_SEGDDL);
+                         MODE == MODE_SEGDDL || MODE == MODE_SEGSPL || MODE == MODE_SEGGRPSPL);
+  constexpr bool SPLIT = (MODE == MODE_SEGSPL || MODE == MODE_SEGGRPSPL);   // k3 line filter (SCI / XCI / MCI)
   constexpr bool LG = (MODE == MODE_SEGLG);   // literal Eq. 22 gain products (NEXT-4b)
   constexpr bool DEDUP = (MODE == MODE_SEGDD || MODE == MODE_SEGDDL);
   constexpr bool DEDUPL = (MODE == MODE_SEGDDL);   // closed-form phased-array factor for runs > 32 spans
   Smem sm;
-  constexpr bool grouped = (MODE == MODE_SEGGRP);   // chain groups (R9): the segment mode when some
+  constexpr bool grouped = mode_grouped(MODE);   // chain groups (R9): the segment mode when some
                                                      // group holds more than one chain
   smem_layout(p.tstride, p.tw, p.N, COH, grouped, smem_raw, &sm);
   const int tid = threadIdx.x;
@@ -825,7 +835,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
   for (int seg0 = 0; seg0 < J; seg0 += LINE_CAP) {
     const int nl = min(LINE_CAP, J - seg0);
     // ---- line scan (gates, point counts) and order-preserving compaction of supported lines
-    const int4 tot = scan_lines(p, sm, seg0, nl, N, a, b, inv_a, k1, k2, C, g);
+    const int4 tot = scan_lines<SPLIT>(p, sm, seg0, nl, N, a, b, inv_a, SPLIT ? rd.kappa : 0, k1, k2, flags, C, g);
     const int S = tot.x, NP = tot.y;
     if (tid == 0) sm.sl_start[S] = NP;
     if (COH) {
@@ -1276,7 +1286,7 @@ integrand_kernel(const KParams p, const int* __restrict__ list) {
 
 template <bool COH, int MODE>
 static int set_smem(int tstride, int tw, int N) {
-  const size_t smem = integrand_smem_bytes(tstride, tw, N, COH, MODE == MODE_SEGGRP);
+  const size_t smem = integrand_smem_bytes(tstride, tw, N, COH, mode_grouped(MODE));
   return cudaFuncSetAttribute(integrand_kernel<COH, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)smem) == cudaSuccess ? 0 : -1;
 }
@@ -1291,6 +1301,8 @@ int integrand_prepare(int mode, int tstride, int tw, int N) {
   switch (mode) {
     case MODE_SEGMENT: return prepare_mode<MODE_SEGMENT>(tstride, tw, N);
     case MODE_SEGGRP: return prepare_mode<MODE_SEGGRP>(tstride, tw, N);
+    case MODE_SEGSPL: return prepare_mode<MODE_SEGSPL>(tstride, tw, N);
+    case MODE_SEGGRPSPL: return prepare_mode<MODE_SEGGRPSPL>(tstride, tw, N);
     case MODE_SEG32: return prepare_mode<MODE_SEG32>(tstride, tw, N);
     case MODE_SEGDD: return prepare_mode<MODE_SEGDD>(tstride, tw, N);
     case MODE_SEGDDL: return prepare_mode<MODE_SEGDDL>(tstride, tw, N);
@@ -1303,7 +1315,7 @@ int integrand_prepare(int mode, int tstride, int tw, int N) {
 
 template <bool COH, int MODE>
 static int launch_one(const KParams& p, const int* list, long long n_list, cudaStream_t st) {
-  const size_t smem = integrand_smem_bytes(p.tstride, p.tw, p.N, COH, MODE == MODE_SEGGRP);
+  const size_t smem = integrand_smem_bytes(p.tstride, p.tw, p.N, COH, mode_grouped(MODE));
   auto kern = integrand_kernel<COH, MODE>;
   const long long max_grid = 0x7fffffffLL;
   for (long long off = 0; off < n_list; off += max_grid) {
@@ -1321,6 +1333,8 @@ int launch_integrand(const KParams& p, const int* list, long long n_list, bool c
   if (coherent) {
     if (p.mode == MODE_SEGMENT) return launch_one<true, MODE_SEGMENT>(p, list, n_list, st);
     if (p.mode == MODE_SEGGRP) return launch_one<true, MODE_SEGGRP>(p, list, n_list, st);
+    if (p.mode == MODE_SEGSPL) return launch_one<true, MODE_SEGSPL>(p, list, n_list, st);
+    if (p.mode == MODE_SEGGRPSPL) return launch_one<true, MODE_SEGGRPSPL>(p, list, n_list, st);
     if (p.mode == MODE_SEG32) return launch_one<true, MODE_SEG32>(p, list, n_list, st);
     if (p.mode == MODE_SEGDD) return launch_one<true, MODE_SEGDD>(p, list, n_list, st);
     if (p.mode == MODE_SEGDDL) return launch_one<true, MODE_SEGDDL>(p, list, n_list, st);
@@ -1331,6 +1345,8 @@ int launch_integrand(const KParams& p, const int* list, long long n_list, bool c
   }
   if (p.mode == MODE_SEGMENT) return launch_one<false, MODE_SEGMENT>(p, list, n_list, st);
   if (p.mode == MODE_SEGGRP) return launch_one<false, MODE_SEGGRP>(p, list, n_list, st);
+  if (p.mode == MODE_SEGSPL) return launch_one<false, MODE_SEGSPL>(p, list, n_list, st);
+  if (p.mode == MODE_SEGGRPSPL) return launch_one<false, MODE_SEGGRPSPL>(p, list, n_list, st);
   if (p.mode == MODE_SEG32) return launch_one<false, MODE_SEG32>(p, list, n_list, st);
   if (p.mode == MODE_SEGDD) return launch_one<false, MODE_SEGDD>(p, list, n_list, st);
   if (p.mode == MODE_SEGDDL) return launch_one<false, MODE_SEGDDL>(p, list, n_list, st);
@@ -1388,6 +1404,51 @@ __global__ void __launch_bounds__(BLOCK) reduce_kernel(const RParams p) {
     p.eta[ci] = e;
     p.npts[ci] = red[5][0];
   }
+}
+
+// SCI / XCI / MCI parts of eta (ISRS_EGN_FLAG_SPLIT): every region entry of the split work list
+// holds islands of ONE class -- the number of distinct interfering channels among (k1, k2, k3): those of
+// (k1, k2), plus one for a K3_OUT entry (k3 is none of kappa, k1, k2) -- so its Eq. 15 contribution goes
+// to that class; fixed-tree sum per COI in canonical order, Eq. 11 scale.  split_out [n_coi][3].
+__global__ void __launch_bounds__(BLOCK) reduce_split_kernel(const RParams p, double* __restrict__ split_out) {
+  __shared__ double red[3][BLOCK];
+  const int ci = blockIdx.x;
+  const int kappa = p.coi[ci];
+  const long long r0 = max(p.coi_off[ci], p.r_lo), r1 = min(p.coi_off[ci + 1], p.r_hi);
+  double acc[3] = {0, 0, 0};
+  for (long long r = r0 + threadIdx.x; r < r1; r += BLOCK) {
+    const RegionDesc rd = p.desc[r];
+    const double* q = p.partials + (size_t)r * 6;
+    const double G1 = p.G[rd.k1], G2 = p.G[rd.k2], R1 = p.R[rd.k1], R2 = p.R[rd.k2];
+    const double ph1 = p.phi[rd.k1], ph2 = p.phi[rd.k2], ps1 = p.psi[rd.k1];
+    double t = 16.0 / 27.0 * G1 * G2 * q[0];
+    t += 16.0 / 27.0 * ph1 * G1 * G1 * G2 * q[1] / R1;
+    t += 32.0 / 81.0 * ph2 * G2 * G2 * G1 * q[2] / R2;
+    t += 16.0 / 81.0 * ph1 * G1 * G1 * q[3] / R1;
+    t += 16.0 / 81.0 * ps1 * G1 * G1 * G1 * q[4] / (R1 * R1);
+    const int nint = (rd.k1 != kappa) + (rd.k2 != kappa && rd.k2 != rd.k1) + ((rd.flags & K3_OUT) ? 1 : 0);
+    acc[min(nint, 2)] += t;
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) red[k][threadIdx.x] = acc[k];
+  __syncthreads();
+  for (int s = BLOCK / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double Pk = p.P[kappa];
+    const double scale = p.R[kappa] / (Pk * Pk * Pk) * p.inv_fs;
+    for (int k = 0; k < 3; ++k) split_out[(size_t)ci * 3 + k] = __dmul_rn(red[k][0], scale);
+  }
+}
+
+int launch_reduce_split(const RParams& p, double* split_out, void* stream) {
+  if (p.n_coi <= 0) return 0;
+  reduce_split_kernel<<<p.n_coi, BLOCK, 0, (cudaStream_t)stream>>>(p, split_out);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 // Multi-GPU combine: the per-COI sums of every shard, added in fixed rank order

@@ -758,3 +758,92 @@ def test_mirror_mode_fp32(isrs):
     e_o, _ = egn.eta(link)
     e_g, _ = gpu_eta(isrs, link, precision=32, flags=isrs.FLAG_MIRROR)
     assert np.all(np.abs(10 * np.log10(e_g / e_o)) <= 1e-3)
+
+
+# ---------------------------------------------------------------- SCI / XCI / MCI split (ISRS_EGN_FLAG_SPLIT)
+
+def _split_links():
+    d = {k: tiny_link(**TINY[k]) for k in ("uniform_64gbd_2span", "three_islands_96gbd", "mixed_rates_guard",
+                                           "touching_bands", "random_spans_multiclass", "single_channel_N64",
+                                           "long_link_chained", "ragged_chunks_N34")}
+    d["two_chain_groups"] = two_chain_groups_link()          # MODE_SEGGRPSPL
+    for seed in range(8):
+        kw, dz = random_tiny_kwargs(seed)
+        d[f"random{seed}"] = tiny_link(**kw).with_(delta_z_m=dz)
+    return d
+
+
+SPLIT_LINKS = _split_links()
+
+
+def _check_split(isrs, link, f_samples=0):
+    e_o, t_o, s_o = egn.eta(link, split=True, f_samples=f_samples)
+    with isrs.Engine(link, flags=isrs.FLAG_SPLIT, f_samples=f_samples) as e:
+        eta, parts, terms = e.nli_split(terms=True)
+        torch.cuda.synchronize()
+        assert e.work() == e.planned_work()
+        assert e.last_launch_count() <= 4
+    eta, parts, terms = eta.cpu().numpy(), parts.cpu().numpy(), terms.cpu().numpy()
+    assert np.all(np.abs(eta - e_o) <= TOL_ETA * e_o), np.abs(eta - e_o) / e_o
+    assert np.all(np.abs(parts - s_o) <= TOL_ETA * e_o[:, None]), (parts, s_o)
+    assert np.all(np.abs(parts.sum(axis=1) - eta) <= 1e-13 * eta)
+    assert np.all(np.abs(terms - t_o) <= TOL_ETA * np.abs(t_o).sum(axis=1, keepdims=True))
+    if link.n_ch == 1:
+        assert np.all(parts[:, 1:] == 0.0)
+    if link.n_ch == 2:
+        assert np.all(parts[:, 2] == 0.0)
+    e_n, _ = gpu_eta(isrs, link, f_samples=f_samples)         # the unsplit work list: same eta
+    assert np.all(np.abs(eta - e_n) <= 1e-12 * e_n)
+
+
+@pytest.mark.parametrize("name", sorted(SPLIT_LINKS))
+def test_sci_xci_mci_split_parity(isrs, name):
+    """eta's SCI / XCI / MCI parts against the oracle's island-by-island classification (pin P17),
+    <= 1e-10 of eta; parts sum to eta; eta equals the unsplit evaluation; the planner's point count of the
+    split work list equals the kernels'."""
+    _check_split(isrs, SPLIT_LINKS[name])
+
+
+def test_sci_xci_mci_split_3d_and_errors(isrs):
+    link = tiny_link(**TINY["three_islands_96gbd"])
+    _check_split(isrs, link, f_samples=2)
+    with isrs.Engine(link) as e:                               # not created with FLAG_SPLIT
+        with pytest.raises(isrs.IsrsEgnError):
+            e.nli_split()
+    for bad in (isrs.FLAG_DEDUP, isrs.FLAG_MIRROR, isrs.FLAG_LITERAL_GAIN, isrs.FLAG_UNIT_LINK):
+        with pytest.raises(isrs.IsrsEgnError):
+            isrs.Engine(link, flags=isrs.FLAG_SPLIT | bad)
+    with pytest.raises(isrs.IsrsEgnError):
+        isrs.Engine(link, flags=isrs.FLAG_SPLIT, precision=32)
+    with isrs.Engine(link, flags=isrs.FLAG_SPLIT) as e:
+        with pytest.raises(isrs.IsrsEgnError):
+            e.nli_shard(0, 2)
+        ref, _ = gpu_eta(isrs, link)
+        assert np.all(np.abs(e.nli().cpu().numpy() - ref) <= 1e-12 * ref)     # plain nli on a split handle
+        e.nli(coi=[1])
+        torch.cuda.synchronize()
+        with isrs.Engine(link) as e0:
+            e0.nli(coi=[1])
+            torch.cuda.synchronize()
+            q = [(1, 1, 1), (1, 0, 1), (1, 0, 2), (1, 2, 2)]
+            a, b = e.region_partials(q), e0.region_partials(q)   # a region's two entries are summed
+            assert np.allclose(a[:, :5], b[:, :5], rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("cfg,coi", [("c2", [0, 19, 39]), ("c3", [0, 50, 99]), ("c4", [0, 40, 79]), ("c5", [100])])
+def test_sci_xci_mci_split_full_size(isrs, cfg, coi):
+    """At full size: eta of the split work list = eta of the headline path (<= 1e-12), the parts sum to it,
+    and every class is populated (MCI dominates the count of regions, SCI is one island)."""
+    link = bj_config(cfg)
+    with isrs.Engine(link) as e:
+        ref = e.nli(coi=coi).cpu().numpy()
+        ms0 = e.last_kernel_ms()[0][3]
+    with isrs.Engine(link, flags=isrs.FLAG_SPLIT) as e:
+        eta, parts = e.nli_split(coi=coi)
+        eta, parts = eta.cpu().numpy(), parts.cpu().numpy()
+        ms1 = e.last_kernel_ms()[0][3]
+    print(f"\n{cfg} split: integrand {ms1:.1f} ms vs {ms0:.1f} ms unsplit; SCI/XCI/MCI shares "
+          f"{np.round(parts / eta[:, None], 4).tolist()}")
+    assert np.all(np.abs(eta - ref) <= 1e-12 * ref)
+    assert np.all(np.abs(parts.sum(axis=1) - eta) <= 1e-13 * eta)
+    assert np.all(parts > 0)
