@@ -363,6 +363,24 @@ MUTANTS.update({
 })
 
 
+def _apply_class_ignores_k3(fwm, isrs, link, egn):
+    def nli_class(kappa, k1, k2, k3):
+        return min(2, len({k1, k2} - {kappa}))                  # slip: k3 not counted
+    egn.nli_class = nli_class
+
+
+def _apply_class_counts_slots(fwm, isrs, link, egn):
+    def nli_class(kappa, k1, k2, k3):
+        return min(2, sum(k != kappa for k in (k1, k2, k3)) - 1 + (k1 == k2 == k3 == kappa))   # slip: slots, not channels
+    egn.nli_class = nli_class
+
+
+MUTANTS.update({
+    "nli_class_ignores_k3": _apply_class_ignores_k3,
+    "nli_class_counts_slots": _apply_class_counts_slots,
+})
+
+
 def apply(name):
     from oracle import egn, fwm, isrs, link
     MUTANTS[name](fwm, isrs, link, egn)

@@ -73,12 +73,23 @@ MUTANTS = {
                        "dedup closed form: phase e^{i G chi L / 2} instead of e^{i (G-1) chi L / 2}"),
     "dedupl_amp_cos": ("kernels.cu", "const double amp = sg / s1;", "const double amp = sg / c1;",
                        "dedup closed form: sin(G chi L/2) / cos(chi L/2)"),
+    # ---- SCI / XCI / MCI split (ISRS_EGN_FLAG_SPLIT)
+    # (dropping `c == kappa` instead is an EQUIVALENT mutant -- it survived, profiles/r02zx_*: a split entry has
+    # kappa in {k1, k2} or k1 == k2 = j, and an island (j, j, kappa) cannot exist between non-overlapping bands:
+    # |f3 - f_kappa| >= 2 |f_j - f_kappa| - R_j >= R_kappa > R_kappa / 2)
+    "split_filter_k2": ("kernels.cu", "const bool in = (c == kappa || c == k1 || c == k2);",
+                        "const bool in = (c == kappa || c == k1);",
+                        "split line filter: k3 = k2 not counted among the region's own channels"),
+    "split_out_class": ("kernels.cu", "+ ((rd.flags & K3_OUT) ? 1 : 0);", "+ ((rd.flags & K3_IN) ? 1 : 0);",
+                        "split reduce: the K3_IN entry, not the K3_OUT one, counts one more interferer"),
+    "split_class_k2": ("kernels.cu", "(rd.k2 != kappa && rd.k2 != rd.k1)", "(rd.k2 != kappa)",
+                       "split reduce: k1 = k2 = j counted as two interferers"),
 }
 
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fvisibility=hidden", "-shared", "--expt-relaxed-constexpr"]
 TESTS = ("tiny or edge or random_links or c1_full or streams or planned_work or chain_groups or (golden and c2_eta) "
-         "or dedup_closed_form")
+         "or dedup_closed_form or (split and not full_size)")
 
 
 def _selected():
