@@ -24,12 +24,15 @@ def main():
         tiny_link(n_ch=3, rates_gbd=(96,), spacing_ghz=100.0, n_span=12, grid_n=8, fmts=("16qam",)),
     ]
     opts = [dict(), dict(precision=32), dict(flags=isrs.FLAG_DEDUP), dict(flags=isrs.FLAG_LITERAL_GAIN),
-            dict(mu_mode=isrs.MU_MACLAURIN), dict(f_samples=2), dict(flags=isrs.FLAG_NO_CHAIN)]
+            dict(mu_mode=isrs.MU_MACLAURIN), dict(f_samples=2), dict(flags=isrs.FLAG_NO_CHAIN),
+            dict(flags=isrs.FLAG_SPLIT), dict(flags=isrs.FLAG_MIRROR)]
     n = 0
     for li, link in enumerate(links):
         for o in (opts if li != 2 else opts[:1]):
             with isrs.Engine(link, **o) as e:
                 eta, _ = e.nli(terms=True)
+                if o.get("flags") == isrs.FLAG_SPLIT:
+                    e.nli_split()
                 torch.cuda.synchronize()
                 assert torch.isfinite(eta).all()
                 n += 1
