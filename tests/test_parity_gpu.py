@@ -847,3 +847,25 @@ def test_sci_xci_mci_split_full_size(isrs, cfg, coi):
     assert np.all(np.abs(eta - ref) <= 1e-12 * ref)
     assert np.all(np.abs(parts.sum(axis=1) - eta) <= 1e-13 * eta)
     assert np.all(parts > 0)
+
+
+@pytest.mark.parametrize("cfg,kappa", [("c2", 20), ("c3", 50), ("c4", 40), ("c5", 100)])
+def test_sci_part_full_size_matches_the_oracle_island(isrs, cfg, kappa):
+    """The split's values (not only their sum) at full size: the SCI part of a COI is the single island
+    (kappa, kappa, kappa), which the literal oracle evaluates on its own in seconds -- at 96 GBd on
+    100 GHz (c3, c5) the same region also holds the kappa3 = kappa +- 1 islands, which must NOT be in it."""
+    link = bj_config(cfg)
+    c = egn.canonicalize(link)
+    isls = egn.region_islands(c, kappa, kappa, kappa, "closed", egn._needed_terms(c, kappa, kappa))
+    own = [i for i in isls if i["k3"] == kappa]
+    assert len(own) == 1 and (cfg in ("c2", "c4") or len(isls) == 3)
+    scale = c.R[kappa] / c.P[kappa] ** 3
+    sci = egn.island_contributions(c, kappa, kappa, own[0]).sum() * scale
+    others = sum(egn.island_contributions(c, kappa, kappa, i).sum() for i in isls if i["k3"] != kappa) * scale
+    with isrs.Engine(link, flags=isrs.FLAG_SPLIT) as e:
+        eta, parts = e.nli_split(coi=[kappa])
+        eta, parts = eta.cpu().numpy(), parts.cpu().numpy()
+    rel = abs(parts[0, 0] - sci) / sci
+    print(f"\n{cfg} COI {kappa}: SCI oracle {sci:.6e} gpu {parts[0, 0]:.6e} rel {rel:.1e}; the region's other "
+          f"islands (XCI) are {others / sci:.3%} of it")
+    assert rel <= TOL_ETA
